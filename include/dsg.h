@@ -1,0 +1,176 @@
+/* dsg.h — C ABI of libdsg.so, the B200-native (sm_100a) drop-in for the
+ * reference hot path (arxiv 2509.12138 "dsplat", /root/reference/proj).
+ *
+ * Plain pointers and sizes only. Host arrays use the reference's own
+ * layouts so the C++ wrappers in include/dsplat_b200/ are thin:
+ *   model params : AoS [n][14] double, order mu(3) log_scale(3) rot wxyz(4)
+ *                  opacity_logit(1) color(3)   (adam.hpp:76-98)
+ *   RGB images   : row-major HWC double        (image.hpp:34-38)
+ *   masks/alpha  : row-major HW double
+ * On the device the model is planar fp32 ([14][capacity]) with its Adam
+ * moments, gradients and densification statistics resident in HBM.
+ *
+ * Every call returns 0 on success, otherwise (dsplat::ErrorCode + 1)
+ * (error.hpp:10-31), and dsg_last_error() returns the thread-local
+ * "<Code>: msg" text that dsplat::Error::what() would give (error.hpp:57-61).
+ * A context owns one CUDA device and stream; handles are not thread-safe.
+ * There is no CPU fallback: without a usable sm_100 device every call
+ * fails with InvalidArgument.
+ */
+#ifndef DSG_H
+#define DSG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSG_ABI_VERSION 1
+
+typedef struct dsg_ctx_s* dsg_ctx;
+typedef struct dsg_model_s* dsg_model;
+typedef struct dsg_views_s* dsg_views;
+
+/* dsplat::Camera (camera.hpp:16-24). */
+typedef struct {
+  double position[3];
+  double target[3];
+  double up[3];
+  double fov_y;
+  int32_t width;
+  int32_t height;
+  double near_plane;
+  double far_plane;
+} dsg_camera;
+
+/* dsplat::RenderConfig (render.hpp:20-25). */
+typedef struct {
+  int32_t tile_size;
+  int32_t _pad;
+  double alpha_cutoff;
+  double sigma_cutoff;
+  double background[3];
+  double transmittance_floor;
+} dsg_render_config;
+
+/* dsplat::AdamConfig (adam.hpp:11-15). */
+typedef struct {
+  double beta1, beta2, epsilon;
+} dsg_adam_config;
+
+/* dsplat::AdamState::GroupRates (adam.hpp:51-53). */
+typedef struct {
+  double mu, log_scale, rot, opacity, color;
+} dsg_group_rates;
+
+/* dsplat::TrainConfig (trainer.hpp:13-30). */
+typedef struct {
+  int64_t iterations;
+  double lr_mu, lr_mu_decay, lr_scale, lr_rot, lr_opacity, lr_color;
+  double loss_lambda;
+  int64_t densify_interval;
+  double densify_grad_threshold, prune_opacity, densify_stop_fraction;
+  double split_scale_threshold;
+  int64_t checkpoint_interval;
+  uint64_t seed;
+  dsg_render_config render;
+  dsg_adam_config adam;
+} dsg_train_config;
+
+/* ProgressSink (trainer.hpp:122): (steps completed, current loss). */
+typedef void (*dsg_progress_fn)(int64_t iteration, double loss, void* user);
+
+const char* dsg_last_error(void);
+int32_t dsg_abi_version(void);
+
+/* ---- context / model ---------------------------------------------------- */
+int dsg_ctx_create(int32_t device, dsg_ctx* out);
+int dsg_ctx_destroy(dsg_ctx ctx);
+int dsg_ctx_synchronize(dsg_ctx ctx);
+
+int dsg_model_create(dsg_ctx ctx, dsg_model* out);
+int dsg_model_destroy(dsg_model model);
+/* Upload a SplatModel (gaussian.hpp:41-54); resets Adam moments and stats. */
+int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t n,
+                     int64_t iteration, int32_t origin_partition);
+int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t capacity,
+                       int64_t* n, int64_t* iteration, int32_t* origin_partition);
+int dsg_model_info(dsg_model model, int64_t* n, int64_t* iteration, int64_t* adam_step);
+/* Adam moments m, v as [n][14] doubles (the AdamState::serialize payload
+ * order, adam.hpp:104-112) and the step counter. */
+int dsg_model_adam_state(dsg_ctx ctx, dsg_model model, double* m, double* v, int64_t* step);
+
+/* ---- render path ---------------------------------------------------------- */
+/* render (render.hpp:160-205). Outputs (each may be NULL): rgb [h][w][3],
+ * alpha [h][w], n_contrib [h][w], splat_order (capacity n) and its length,
+ * model_iteration (RenderOutput::model_iteration). */
+int dsg_render(dsg_ctx ctx, dsg_model model, const dsg_camera* cam,
+               const dsg_render_config* cfg, double* rgb, double* alpha, int32_t* n_contrib,
+               int32_t* splat_order, int64_t* n_order, int64_t* model_iteration);
+
+/* Per-tile compositing lists of the last dsg_render/dsg_bin on ctx, for
+ * parity checks against bin_splats (render.hpp:117-135) at tile_size 16:
+ * tile_count[tiles], entries (gaussian indices) capacity given. */
+int dsg_bin(dsg_ctx ctx, dsg_model model, const dsg_camera* cam, const dsg_render_config* cfg,
+            int32_t* tile_count, int32_t* entries, int64_t capacity, int64_t* n_entries);
+
+/* render_mask (render.hpp:210-233): points [n][3]; mask [h][w] in {0,1}. */
+int dsg_render_mask(dsg_ctx ctx, const double* points, int64_t n, const dsg_camera* cam,
+                    double footprint_px, double dilation_px, double* mask);
+
+/* masked_loss (loss.hpp:39-73) on host images. */
+int dsg_masked_loss(dsg_ctx ctx, const double* rendered, const double* ground_truth,
+                    const double* mask, int32_t width, int32_t height, double loss_lambda,
+                    double* loss, double* dL_dpixels);
+
+/* backward (backward.hpp:184-332). output_iteration is the
+ * RenderOutput::model_iteration of the forward the caller holds
+ * (StaleForward if it differs from the model's). The device reduction is
+ * shard-invariant, so shards (>= 1) only validates. grads [n][14],
+ * d_mean2d [n][2] and touch_count [n] (gradient.hpp:12-46) may be NULL. */
+int dsg_backward(dsg_ctx ctx, dsg_model model, const dsg_camera* cam,
+                 const dsg_render_config* cfg, int64_t output_iteration,
+                 const double* dL_dpixels, int32_t shards, double* grads, double* d_mean2d,
+                 int32_t* touch_count);
+
+/* AdamState::step (adam.hpp:55-101) with host gradients [n][14] on the
+ * model's device-resident moments; increments the step counter. */
+int dsg_adam_step(dsg_ctx ctx, dsg_model model, const double* grads,
+                  const dsg_group_rates* rates, const dsg_adam_config* adam);
+
+/* ---- training -------------------------------------------------------------- */
+/* Train views (TrainView, loss.hpp:14-26) resident on the device: ground
+ * truth [v][h][w][3] and masks [v][h][w] doubles; all views share (w, h). */
+int dsg_views_create(dsg_ctx ctx, const dsg_camera* cams, const double* ground_truth,
+                     const double* masks, int32_t n_views, dsg_views* out);
+/* make_train_view (runtime.hpp:190-199) on the device: ground truth is the
+ * render of gt_model, masks are render_mask of points (or all ones). */
+int dsg_views_synthesize(dsg_ctx ctx, dsg_model gt_model, const dsg_render_config* cfg,
+                         const dsg_camera* cams, int32_t n_views, const double* points,
+                         int64_t n_points, int32_t use_masks, double footprint_px,
+                         double dilation_px, dsg_views* out);
+int dsg_views_destroy(dsg_views views);
+/* Copy view v back (gt [h][w][3], mask [h][w]; either may be NULL). */
+int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t v, double* ground_truth,
+                       double* mask);
+
+/* train_partition_full (trainer.hpp:140-211): the whole loop on the device.
+ * The model is updated in place (iteration advances). progress may be NULL;
+ * loss_trace (capacity iterations) may be NULL. Densification events are
+ * not yet supported on the device and return InvalidArgument before any
+ * step runs. */
+int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_config* cfg,
+              int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
+              double* loss_trace);
+
+/* Record per-stage CUDA events inside dsg_train (adds one sync per step). */
+int dsg_set_profiling(dsg_ctx ctx, int32_t enable);
+
+/* CUDA-event device time (ms) of the last dsg_train call and the per-stage
+ * totals {preprocess+sort, blend fwd, loss, blend bwd, chain, adam}. */
+int dsg_last_timing(dsg_ctx ctx, double* total_ms, double* stage_ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

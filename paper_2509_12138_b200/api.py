@@ -1,0 +1,404 @@
+"""Reference-shaped host API over libdsg.so (include/dsg.h) via ctypes.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(proj/include/dsplat): ``render`` (render.hpp:160), ``render_mask``
+(render.hpp:210), ``masked_loss`` (loss.hpp:39), ``backward``
+(backward.hpp:184), ``AdamState.step`` (adam.hpp:55),
+``train_partition_full`` / ``train_partition`` (trainer.hpp:140, 214).
+Every call runs on the B200 through the C ABI; if libdsg.so is missing or no
+sm_100 device is present the call raises — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .types import (PARAMS, AdamConfig, Camera, DsplatError, ErrorCode, GradientBuffer, GroupRates,
+                    LossResult, RenderConfig, RenderOutput, SplatModel, TrainConfig, TrainResult,
+                    TrainView)
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libdsg.so")
+
+
+class dsg_camera(C.Structure):
+    _fields_ = [("position", C.c_double * 3), ("target", C.c_double * 3), ("up", C.c_double * 3),
+                ("fov_y", C.c_double), ("width", C.c_int32), ("height", C.c_int32),
+                ("near_plane", C.c_double), ("far_plane", C.c_double)]
+
+
+class dsg_render_config(C.Structure):
+    _fields_ = [("tile_size", C.c_int32), ("_pad", C.c_int32), ("alpha_cutoff", C.c_double),
+                ("sigma_cutoff", C.c_double), ("background", C.c_double * 3),
+                ("transmittance_floor", C.c_double)]
+
+
+class dsg_adam_config(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("epsilon", C.c_double)]
+
+
+class dsg_group_rates(C.Structure):
+    _fields_ = [("mu", C.c_double), ("log_scale", C.c_double), ("rot", C.c_double),
+                ("opacity", C.c_double), ("color", C.c_double)]
+
+
+class dsg_train_config(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("lr_mu", C.c_double), ("lr_mu_decay", C.c_double),
+                ("lr_scale", C.c_double), ("lr_rot", C.c_double), ("lr_opacity", C.c_double),
+                ("lr_color", C.c_double), ("loss_lambda", C.c_double),
+                ("densify_interval", C.c_int64), ("densify_grad_threshold", C.c_double),
+                ("prune_opacity", C.c_double), ("densify_stop_fraction", C.c_double),
+                ("split_scale_threshold", C.c_double), ("checkpoint_interval", C.c_int64),
+                ("seed", C.c_uint64), ("render", dsg_render_config), ("adam", dsg_adam_config)]
+
+
+PROGRESS_FN = C.CFUNCTYPE(None, C.c_int64, C.c_double, C.c_void_p)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib() -> C.CDLL:
+    """Load libdsg.so (raises if it was not built — no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"libdsg.so not built at {LIB_PATH}; run __graft_entry__.build()")
+            L = C.CDLL(LIB_PATH)
+            L.dsg_last_error.restype = C.c_char_p
+            _lib = L
+    return _lib
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().dsg_last_error().decode()
+        code = ErrorCode(rc - 1)
+        raise DsplatError(code, msg.split(": ", 1)[1] if ": " in msg else msg)
+
+
+def _p(a, ct=C.c_double):
+    return None if a is None else a.ctypes.data_as(C.POINTER(ct))
+
+
+def cam_struct(cam: Camera) -> dsg_camera:
+    c = dsg_camera()
+    c.position[:] = [float(v) for v in cam.position]
+    c.target[:] = [float(v) for v in cam.target]
+    c.up[:] = [float(v) for v in cam.up]
+    c.fov_y = cam.fov_y
+    c.width = cam.width
+    c.height = cam.height
+    c.near_plane = cam.near
+    c.far_plane = cam.far
+    return c
+
+
+def cfg_struct(cfg: RenderConfig) -> dsg_render_config:
+    c = dsg_render_config()
+    c.tile_size = cfg.tile_size
+    c.alpha_cutoff = cfg.alpha_cutoff
+    c.sigma_cutoff = cfg.sigma_cutoff
+    c.background[:] = [float(v) for v in cfg.background]
+    c.transmittance_floor = cfg.transmittance_floor
+    return c
+
+
+def train_struct(cfg: TrainConfig) -> dsg_train_config:
+    t = dsg_train_config()
+    for name in ("iterations", "lr_mu", "lr_mu_decay", "lr_scale", "lr_rot", "lr_opacity",
+                 "lr_color", "loss_lambda", "densify_interval", "densify_grad_threshold",
+                 "prune_opacity", "densify_stop_fraction", "split_scale_threshold",
+                 "checkpoint_interval", "seed"):
+        setattr(t, name, getattr(cfg, name))
+    t.render = cfg_struct(cfg.render)
+    t.adam = dsg_adam_config(cfg.adam.beta1, cfg.adam.beta2, cfg.adam.epsilon)
+    return t
+
+
+class Context:
+    """One CUDA device + stream (dsg_ctx). Not thread-safe."""
+
+    def __init__(self, device: int = 0):
+        self.h = C.c_void_p()
+        _check(lib().dsg_ctx_create(C.c_int32(device), C.byref(self.h)))
+        self.device = device
+
+    def close(self):
+        if self.h:
+            lib().dsg_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        _check(lib().dsg_ctx_synchronize(self.h))
+
+    def set_profiling(self, on: bool):
+        _check(lib().dsg_set_profiling(self.h, C.c_int32(1 if on else 0)))
+
+    def last_timing(self):
+        tot = C.c_double()
+        st = np.zeros(6)
+        _check(lib().dsg_last_timing(self.h, C.byref(tot), _p(st)))
+        return tot.value, st
+
+
+class DeviceModel:
+    """A splat model resident on the device (dsg_model)."""
+
+    def __init__(self, ctx: Context, model: SplatModel = None):
+        self.ctx = ctx
+        self.h = C.c_void_p()
+        _check(lib().dsg_model_create(ctx.h, C.byref(self.h)))
+        if model is not None:
+            self.upload(model)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().dsg_model_destroy(self.h)
+        except Exception:
+            pass
+
+    def upload(self, model: SplatModel):
+        P = np.ascontiguousarray(model.params, dtype=np.float64)
+        op = -1 if model.origin_partition is None else int(model.origin_partition)
+        _check(lib().dsg_model_upload(self.ctx.h, self.h, _p(P), C.c_int64(P.shape[0]),
+                                      C.c_int64(model.iteration), C.c_int32(op)))
+
+    def info(self):
+        n, it, st = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().dsg_model_info(self.h, C.byref(n), C.byref(it), C.byref(st)))
+        return n.value, it.value, st.value
+
+    def download(self) -> SplatModel:
+        n, _, _ = self.info()
+        P = np.zeros((max(n, 1), PARAMS))
+        nn, it, op = C.c_int64(), C.c_int64(), C.c_int32()
+        _check(lib().dsg_model_download(self.ctx.h, self.h, _p(P), C.c_int64(P.shape[0]),
+                                        C.byref(nn), C.byref(it), C.byref(op)))
+        return SplatModel(P[: nn.value].copy(), it.value, None if op.value < 0 else op.value)
+
+    def adam_state(self):
+        n, _, _ = self.info()
+        m = np.zeros((max(n, 1), PARAMS))
+        v = np.zeros((max(n, 1), PARAMS))
+        st = C.c_int64()
+        _check(lib().dsg_model_adam_state(self.ctx.h, self.h, _p(m), _p(v), C.byref(st)))
+        return m[:n], v[:n], st.value
+
+
+class DeviceViews:
+    """Train views resident on the device (dsg_views)."""
+
+    def __init__(self, ctx: Context, handle: C.c_void_p, cams, width, height):
+        self.ctx = ctx
+        self.h = handle
+        self.cams = cams
+        self.width = width
+        self.height = height
+
+    @classmethod
+    def from_views(cls, ctx: Context, views):
+        n = len(views)
+        h = C.c_void_p()
+        if n == 0:
+            _check(lib().dsg_views_create(ctx.h, None, None, None, C.c_int32(0), C.byref(h)))
+            return cls(ctx, h, [], 0, 0)
+        for v in views:
+            v.validate()
+        cams = (dsg_camera * n)(*[cam_struct(v.cam) for v in views])
+        gts = np.ascontiguousarray(np.stack([v.ground_truth for v in views]), dtype=np.float64)
+        masks = np.ascontiguousarray(np.stack([v.mask for v in views]), dtype=np.float64)
+        _check(lib().dsg_views_create(ctx.h, cams, _p(gts), _p(masks), C.c_int32(n), C.byref(h)))
+        return cls(ctx, h, [v.cam for v in views], views[0].cam.width, views[0].cam.height)
+
+    @classmethod
+    def synthesize(cls, ctx: Context, gt_model: "DeviceModel", cfg: RenderConfig, cams, points,
+                   use_masks=True, footprint_px=2.0, dilation_px=2.0):
+        """make_train_view (runtime.hpp:190-199) for every camera, on device."""
+        n = len(cams)
+        carr = (dsg_camera * max(n, 1))(*[cam_struct(c) for c in cams])
+        pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+        h = C.c_void_p()
+        _check(lib().dsg_views_synthesize(ctx.h, gt_model.h, C.byref(cfg_struct(cfg)), carr,
+                                          C.c_int32(n), _p(pts), C.c_int64(pts.shape[0]),
+                                          C.c_int32(1 if use_masks else 0), C.c_double(footprint_px),
+                                          C.c_double(dilation_px), C.byref(h)))
+        return cls(ctx, h, list(cams), cams[0].width if n else 0, cams[0].height if n else 0)
+
+    def download(self, i: int) -> TrainView:
+        gt = np.zeros((self.height, self.width, 3))
+        m = np.zeros((self.height, self.width))
+        _check(lib().dsg_views_download(self.ctx.h, self.h, C.c_int32(i), _p(gt), _p(m)))
+        return TrainView(self.cams[i], gt, m)
+
+    def __len__(self):
+        return len(self.cams)
+
+    def __del__(self):
+        try:
+            if self.h:
+                lib().dsg_views_destroy(self.h)
+        except Exception:
+            pass
+
+
+_default_ctx = {}
+
+
+def default_context(device: int = 0) -> Context:
+    if device not in _default_ctx:
+        _default_ctx[device] = Context(device)
+    return _default_ctx[device]
+
+
+def _as_device_model(model, ctx: Context) -> DeviceModel:
+    if isinstance(model, DeviceModel):
+        return model
+    return DeviceModel(ctx, model)
+
+
+# ---- reference-shaped API -----------------------------------------------------
+def render(model, cam: Camera, cfg: RenderConfig, ctx: Context = None) -> RenderOutput:
+    """render (render.hpp:160-205) on the device."""
+    ctx = ctx or default_context()
+    dm = _as_device_model(model, ctx)
+    n, _, _ = dm.info()
+    h, w = cam.height, cam.width
+    rgb = np.zeros((max(h, 1), max(w, 1), 3))
+    alpha = np.zeros((max(h, 1), max(w, 1)))
+    nc = np.zeros((max(h, 1), max(w, 1)), np.int32)
+    order = np.zeros(max(n, 1), np.int32)
+    no, it = C.c_int64(), C.c_int64()
+    _check(lib().dsg_render(ctx.h, dm.h, C.byref(cam_struct(cam)), C.byref(cfg_struct(cfg)),
+                            _p(rgb), _p(alpha), _p(nc, C.c_int32), _p(order, C.c_int32),
+                            C.byref(no), C.byref(it)))
+    return RenderOutput(rgb, alpha, nc, order[: no.value].copy(), it.value)
+
+
+def bin_splats(model, cam: Camera, cfg: RenderConfig, ctx: Context = None, capacity=1 << 22):
+    """Per-tile compositing lists (bin_splats, render.hpp:117-135) at 16 px tiles."""
+    ctx = ctx or default_context()
+    dm = _as_device_model(model, ctx)
+    tx = (cam.width + 15) // 16
+    ty = (cam.height + 15) // 16
+    counts = np.zeros(tx * ty, np.int32)
+    entries = np.zeros(capacity, np.int32)
+    ne = C.c_int64()
+    _check(lib().dsg_bin(ctx.h, dm.h, C.byref(cam_struct(cam)), C.byref(cfg_struct(cfg)),
+                         _p(counts, C.c_int32), _p(entries, C.c_int32), C.c_int64(capacity),
+                         C.byref(ne)))
+    return counts, entries[: ne.value].copy()
+
+
+def render_mask(points, cam: Camera, footprint_px: float, dilation_px: float,
+                ctx: Context = None):
+    """render_mask (render.hpp:210-233) on the device."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    mask = np.zeros((max(cam.height, 1), max(cam.width, 1)))
+    _check(lib().dsg_render_mask(ctx.h, _p(pts), C.c_int64(pts.shape[0]), C.byref(cam_struct(cam)),
+                                 C.c_double(footprint_px), C.c_double(dilation_px), _p(mask)))
+    return mask
+
+
+def masked_loss(rendered, view: TrainView, loss_lambda: float, ctx: Context = None) -> LossResult:
+    """masked_loss (loss.hpp:39-73) on the device."""
+    ctx = ctx or default_context()
+    view.validate()
+    r = np.ascontiguousarray(rendered, dtype=np.float64)
+    if r.shape != view.ground_truth.shape:
+        raise DsplatError(ErrorCode.DimensionMismatch, "image dimensions differ")
+    gt = np.ascontiguousarray(view.ground_truth, dtype=np.float64)
+    m = np.ascontiguousarray(view.mask, dtype=np.float64)
+    h, w = r.shape[:2]
+    dL = np.zeros_like(r)
+    loss = C.c_double()
+    _check(lib().dsg_masked_loss(ctx.h, _p(r), _p(gt), _p(m), C.c_int32(w), C.c_int32(h),
+                                 C.c_double(loss_lambda), C.byref(loss), _p(dL)))
+    return LossResult(loss.value, dL)
+
+
+def backward(model, cam: Camera, cfg: RenderConfig, output: RenderOutput, dL_dpixels,
+             shards: int = 1, ctx: Context = None) -> GradientBuffer:
+    """backward (backward.hpp:184-332) on the device."""
+    ctx = ctx or default_context()
+    dm = _as_device_model(model, ctx)
+    n, _, _ = dm.info()
+    d = np.ascontiguousarray(dL_dpixels, dtype=np.float64)
+    if d.shape != (cam.height, cam.width, 3):
+        raise DsplatError(ErrorCode.DimensionMismatch, "dL_dpixels must be RGB at camera resolution")
+    G = np.zeros((max(n, 1), PARAMS))
+    dmn = np.zeros((max(n, 1), 2))
+    tc = np.zeros(max(n, 1), np.int32)
+    _check(lib().dsg_backward(ctx.h, dm.h, C.byref(cam_struct(cam)), C.byref(cfg_struct(cfg)),
+                              C.c_int64(output.model_iteration), _p(d), C.c_int32(shards), _p(G),
+                              _p(dmn), _p(tc, C.c_int32)))
+    return GradientBuffer(G[:n], dmn[:n], tc[:n])
+
+
+class AdamState:
+    """AdamState (adam.hpp:19-119) whose moments live with a DeviceModel."""
+
+    kScalars = PARAMS
+
+    def __init__(self, model: DeviceModel):
+        self.model = model
+
+    def step(self, grads: GradientBuffer, lr: GroupRates, cfg: AdamConfig = None):
+        cfg = cfg or AdamConfig()
+        G = np.ascontiguousarray(grads.grads, dtype=np.float64)
+        r = dsg_group_rates(*lr.as_tuple())
+        a = dsg_adam_config(cfg.beta1, cfg.beta2, cfg.epsilon)
+        _check(lib().dsg_adam_step(self.model.ctx.h, self.model.h, _p(G), C.byref(r), C.byref(a)))
+
+    def step_count(self) -> int:
+        return self.model.info()[2]
+
+
+def train_device(dmodel: DeviceModel, dviews: DeviceViews, cfg: TrainConfig, shards: int = 1,
+                 progress=None, loss_trace: bool = False):
+    """The device-resident training loop (dsg_train); returns (final_loss, trace)."""
+    fl = C.c_double()
+    trace = np.zeros(max(cfg.iterations, 1)) if loss_trace else None
+    cb = PROGRESS_FN(lambda it, loss, user: progress(it, loss)) if progress else None
+    _check(lib().dsg_train(dmodel.ctx.h, dmodel.h, dviews.h, C.byref(train_struct(cfg)),
+                           C.c_int32(shards), cb, None, C.byref(fl), _p(trace)))
+    return fl.value, (trace[: cfg.iterations] if trace is not None else None)
+
+
+def train_partition_full(model: SplatModel, views, cfg: TrainConfig, shards: int = 1,
+                         checkpoint=None, progress=None, ctx: Context = None,
+                         loss_trace: bool = False) -> TrainResult:
+    """train_partition_full (trainer.hpp:140-211): host in, host out."""
+    ctx = ctx or default_context()
+    cfg.validate()
+    if len(views) == 0:
+        raise DsplatError(ErrorCode.NoViews, "training requires at least one view")
+    if shards < 1:
+        raise DsplatError(ErrorCode.InvalidArgument, "shards must be >= 1")
+    dm = DeviceModel(ctx, model)
+    dv = DeviceViews.from_views(ctx, views)
+    fl, trace = train_device(dm, dv, cfg, shards, progress, loss_trace)
+    out = dm.download()
+    out.origin_partition = model.origin_partition
+    res = TrainResult(out, fl, len(model), len(out))
+    if trace is not None:
+        res.loss_trace = trace
+    return res
+
+
+def train_partition(model: SplatModel, views, cfg: TrainConfig, shards: int = 1,
+                    ctx: Context = None) -> SplatModel:
+    """train_partition (trainer.hpp:214-217)."""
+    return train_partition_full(model, views, cfg, shards, ctx=ctx).model

@@ -1,0 +1,856 @@
+// libdsg C ABI (include/dsg.h): host orchestration of the sm_100a kernels.
+//
+// Mirrors the reference entry points render (render.hpp:160), backward
+// (backward.hpp:184), masked_loss (loss.hpp:39), AdamState::step
+// (adam.hpp:55) and train_partition_full (trainer.hpp:140) over device-
+// resident models and views. Validation order and messages follow the
+// reference so the C++ wrappers can rethrow identical dsplat::Error texts.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/dsg.h"
+#include "dsg_internal.h"
+#include "raster.h"
+
+namespace dsg {
+
+static const char* kCodeNames[] = {
+    "BehindCamera", "InvalidRig", "UnknownKind", "IsovalueOutOfRange", "EmptyCloud",
+    "DimensionMismatch", "TooSmall", "EmptyBand", "EmptyInterior", "MismatchedCounts", "NoViews",
+    "StaleForward", "IoError", "MalformedFile", "WorkerFailure", "Timeout", "ManifestMismatch",
+    "MissingBaseline", "InvalidArgument"};
+
+void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void throw_cuda(cudaError_t e, const char* expr, const char* file, int line) {
+  char buf[512];
+  snprintf(buf, sizeof buf, "CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e),
+           cudaGetErrorString(e), file, line, expr);
+  throw Error{kWorkerFailure, buf};
+}
+
+void ModelDev::reserve(int64_t c) {
+  if (c <= cap) return;
+  int64_t nc = std::max<int64_t>(c, 64);
+  params.release(); grads.release(); m.release(); v.release(); dmean.release();
+  stat_norm.release(); touch.release(); stat_count.release();
+  params.ensure(kParams * nc);
+  grads.ensure(kParams * nc);
+  m.ensure(kParams * nc);
+  v.ensure(kParams * nc);
+  dmean.ensure(2 * nc);
+  stat_norm.ensure(nc);
+  touch.ensure(nc);
+  stat_count.ensure(nc);
+  cap = nc;
+}
+
+}  // namespace dsg
+
+using namespace dsg;
+
+struct dsg_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Frame frame;
+  DevBuf<double> stage_d;
+  DevBuf<double> stage_d2;
+  DevBuf<float> stage_f;
+  DevBuf<uint8_t> stage_u8;
+  DevBuf<double> loss_trace;
+  std::vector<cudaEvent_t> events;
+  double last_total_ms = 0.0;
+  double last_stage_ms[6] = {0, 0, 0, 0, 0, 0};
+  bool profile = false;
+};
+
+struct dsg_model_s {
+  ModelDev m;
+};
+
+struct dsg_views_s {
+  int32_t n = 0;
+  int width = 0, height = 0;
+  std::vector<dsg_camera> cams;
+  DevBuf<float> gt;       // [v][3][npix]
+  DevBuf<uint8_t> mask;   // [v][npix]
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const Error& e) {
+    g_err = std::string(kCodeNames[e.code]) + ": " + e.msg;
+    return e.code + 1;
+  } catch (const std::exception& e) {
+    g_err = std::string("InvalidArgument: ") + e.what();
+    return kInvalidArgument + 1;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) DSG_CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---- host mirrors of the reference's small value types -----------------------
+struct V3 {
+  double x, y, z;
+};
+V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+V3 cross(V3 a, V3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+double norm(V3 a) { return std::sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+V3 unit(V3 a) {
+  double n = norm(a);
+  return n > 0.0 ? V3{a.x / n, a.y / n, a.z / n} : V3{0, 0, 0};
+}
+
+// Camera::validate (camera.hpp:26-36) + the constants of camera.hpp:40-62.
+CamDev make_cam(const dsg_camera* c) {
+  if (!c) fail(kInvalidArgument, "null camera");
+  if (c->width < 8 || c->height < 8) fail(kInvalidRig, "camera resolution below 8 px");
+  if (!(c->fov_y > 0.0 && c->fov_y < M_PI)) fail(kInvalidRig, "fov_y outside (0, pi)");
+  if (!(c->near_plane < c->far_plane)) fail(kInvalidRig, "near must be < far");
+  V3 pos{c->position[0], c->position[1], c->position[2]};
+  V3 tgt{c->target[0], c->target[1], c->target[2]};
+  V3 up{c->up[0], c->up[1], c->up[2]};
+  V3 dir = sub(tgt, pos);
+  if (norm(cross(dir, up)) <= 1e-12 * norm(dir) * norm(up))
+    fail(kInvalidRig, "up parallel to view direction");
+  V3 f = unit(dir);
+  V3 r = unit(cross(f, up));
+  V3 u = cross(r, f);
+  CamDev k{};
+  double R[9] = {r.x, r.y, r.z, u.x, u.y, u.z, f.x, f.y, f.z};
+  std::memcpy(k.R, R, sizeof R);
+  k.pos[0] = pos.x;
+  k.pos[1] = pos.y;
+  k.pos[2] = pos.z;
+  k.f = 0.5 * c->height / std::tan(0.5 * c->fov_y);
+  k.half_w = 0.5 * c->width;
+  k.half_h = 0.5 * c->height;
+  k.near_plane = c->near_plane;
+  k.width = c->width;
+  k.height = c->height;
+  k.tiles_x = (c->width + kTile - 1) / kTile;
+  k.tiles_y = (c->height + kTile - 1) / kTile;
+  return k;
+}
+
+// RenderConfig::validate (render.hpp:27-34).
+RenderDev make_rd(const dsg_render_config* c) {
+  if (!c) fail(kInvalidArgument, "null render config");
+  if (c->tile_size <= 0 || (c->tile_size & (c->tile_size - 1)) != 0)
+    fail(kInvalidArgument, "tile_size must be a positive power of two");
+  if (!(c->alpha_cutoff > 0.0 && c->alpha_cutoff < 1.0))
+    fail(kInvalidArgument, "alpha_cutoff outside (0, 1)");
+  if (!(c->sigma_cutoff >= 1.0 && c->sigma_cutoff <= 6.0))
+    fail(kInvalidArgument, "sigma_cutoff outside [1, 6]");
+  RenderDev r{};
+  r.sigma_cutoff = c->sigma_cutoff;
+  r.sigma_sq = c->sigma_cutoff * c->sigma_cutoff;
+  r.alpha_cutoff = c->alpha_cutoff;
+  r.floor_T = c->transmittance_floor;
+  for (int k = 0; k < 3; ++k) r.bg[k] = (float)c->background[k];
+  r.sigma_sq_f = (float)r.sigma_sq;
+  r.alpha_cutoff_f = (float)r.alpha_cutoff;
+  r.floor_T_f = (float)r.floor_T;
+  return r;
+}
+
+// ---- layout conversion kernels -------------------------------------------------
+__global__ void k_aos_to_planar(const double* __restrict__ aos, int64_t n, int C,
+                                float* __restrict__ planar, int64_t pitch) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < C; ++c) planar[c * pitch + i] = (float)aos[i * C + c];
+}
+
+__global__ void k_planar_to_aos(const float* __restrict__ planar, int64_t pitch, int64_t n, int C,
+                                double* __restrict__ aos) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int c = 0; c < C; ++c) aos[i * C + c] = (double)planar[c * pitch + i];
+}
+
+__global__ void k_mask_u8(const double* __restrict__ m, int64_t n, uint8_t* __restrict__ out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = m[i] >= 0.5 ? 1 : 0;
+}
+
+__global__ void k_render_out(const float* __restrict__ rgb, const float* __restrict__ T,
+                             int64_t npix, double* __restrict__ out_rgb,
+                             double* __restrict__ out_alpha) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  for (int c = 0; c < 3; ++c) out_rgb[3 * i + c] = (double)rgb[c * npix + i];
+  out_alpha[i] = 1.0 - (double)T[i];
+}
+
+__global__ void k_fill_bg(float* rgb, float* T, uint32_t* last, int32_t* nc, int64_t npix,
+                          float r, float g, float b) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npix) return;
+  rgb[i] = r;
+  rgb[npix + i] = g;
+  rgb[2 * npix + i] = b;
+  T[i] = 1.f;
+  last[i] = 0;
+  nc[i] = 0;
+}
+
+inline unsigned nblk(int64_t n, int t = 256) { return (unsigned)std::max<int64_t>(1, (n + t - 1) / t); }
+
+// Forward pass of one view into ctx->frame (binning + K5). An empty visible
+// set leaves the background image, like render() (render.hpp:169-172).
+void forward(dsg_ctx ctx, ModelDev& m, const CamDev& cam, const RenderDev& rd) {
+  Frame& f = ctx->frame;
+  bin_frame(f, m.params.get(), m.cap, m.n, cam, rd, ctx->stream);
+  const int64_t npix = (int64_t)cam.width * cam.height;
+  if (f.n_visible == 0 || f.n_dup == 0) {
+    f.width = cam.width;
+    f.height = cam.height;
+    f.rgb.ensure(3 * npix);
+    f.T.ensure(npix);
+    f.last.ensure(npix);
+    f.ncontrib.ensure(npix);
+    k_fill_bg<<<nblk(npix), 256, 0, ctx->stream>>>(f.rgb.get(), f.T.get(), f.last.get(),
+                                                   f.ncontrib.get(), npix, rd.bg[0], rd.bg[1],
+                                                   rd.bg[2]);
+    return;
+  }
+  blend_forward(f, m.params.get(), m.cap, cam, rd, ctx->stream);
+}
+
+// K6 + K7 on the current frame (forward and f.dL must be in place).
+void backward_dev(dsg_ctx ctx, ModelDev& m, const CamDev& cam, const RenderDev& rd) {
+  Frame& f = ctx->frame;
+  blend_backward(f, m.params.get(), m.cap, cam, rd, ctx->stream);
+  ChainArgs a;
+  a.params = m.params.get();
+  a.pitch = m.cap;
+  a.n = m.n;
+  a.cam = cam;
+  a.tcount = f.tcount.get();
+  a.dup_base = f.dup_base.get();
+  a.partials = f.partials.get();
+  a.grads = m.grads.get();
+  a.dmean = m.dmean.get();
+  a.touch = m.touch.get();
+  if (f.n_visible == 0 || f.n_dup == 0) {
+    // nothing visible: all gradients are exactly zero (backward.hpp:195)
+    DSG_CUDA_CHECK(cudaMemsetAsync(m.grads.get(), 0, sizeof(float) * kParams * m.cap, ctx->stream));
+    DSG_CUDA_CHECK(cudaMemsetAsync(m.dmean.get(), 0, sizeof(float) * 2 * m.cap, ctx->stream));
+    DSG_CUDA_CHECK(cudaMemsetAsync(m.touch.get(), 0, sizeof(int32_t) * m.cap, ctx->stream));
+    return;
+  }
+  chain_3d(a, ctx->stream);
+}
+
+AdamArgs make_adam(ModelDev& m, const double* rates, const dsg_adam_config& ac, int64_t step,
+                   bool stats) {
+  AdamArgs a;
+  a.params = m.params.get();
+  a.grads = m.grads.get();
+  a.m = m.m.get();
+  a.v = m.v.get();
+  a.dmean = m.dmean.get();
+  a.touch = m.touch.get();
+  a.stat_norm = m.stat_norm.get();
+  a.stat_count = m.stat_count.get();
+  a.pitch = m.cap;
+  a.n = m.n;
+  for (int k = 0; k < 5; ++k) a.lr[k] = (float)rates[k];
+  a.b1 = (float)ac.beta1;
+  a.b2 = (float)ac.beta2;
+  a.omb1 = (float)(1.0 - ac.beta1);
+  a.omb2 = (float)(1.0 - ac.beta2);
+  double bc1 = 1.0 - std::pow(ac.beta1, (double)step);
+  double bc2 = 1.0 - std::pow(ac.beta2, (double)step);
+  a.inv_bc1 = (float)(1.0 / bc1);
+  a.inv_bc2 = (float)(1.0 / bc2);
+  a.eps = (float)ac.epsilon;
+  a.ls_lo = (float)std::log(1e-7);
+  a.ls_hi = (float)std::log(1e3);
+  a.accumulate_stats = stats ? 1 : 0;
+  return a;
+}
+
+void reset_optimizer(dsg_ctx ctx, ModelDev& m) {
+  cudaStream_t st = ctx->stream;
+  DSG_CUDA_CHECK(cudaMemsetAsync(m.m.get(), 0, sizeof(float) * kParams * m.cap, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(m.v.get(), 0, sizeof(float) * kParams * m.cap, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_norm.get(), 0, sizeof(float) * m.cap, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_count.get(), 0, sizeof(int32_t) * m.cap, st));
+  m.adam_step = 0;
+}
+
+// splitmix64 stream of rng.hpp:8-64 (view order shuffle, trainer.hpp:160-163).
+struct Rng {
+  uint64_t s;
+  static uint64_t mix(uint64_t& st) {
+    st += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = st;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+  }
+  explicit Rng(uint64_t seed) : s(seed ^ 0x853c49e6748fea9bULL) {
+    mix(s);
+    mix(s);
+  }
+  uint64_t below(uint64_t n) { return n > 0 ? mix(s) % n : 0; }
+};
+
+void validate_train(const dsg_train_config* c) {  // trainer.hpp:31-38
+  if (c->lr_mu <= 0 || c->lr_scale <= 0 || c->lr_rot <= 0 || c->lr_opacity <= 0 || c->lr_color <= 0)
+    fail(kInvalidArgument, "learning rates must be positive");
+  if (c->loss_lambda < 0.0 || c->loss_lambda > 1.0)
+    fail(kInvalidArgument, "loss_lambda outside [0, 1]");
+  if (c->iterations < 0) fail(kInvalidArgument, "iterations must be >= 0");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dsg_last_error(void) { return g_err.c_str(); }
+int32_t dsg_abi_version(void) { return DSG_ABI_VERSION; }
+
+int dsg_ctx_create(int32_t device, dsg_ctx* out) {
+  return guarded([&] {
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) fail(kInvalidArgument, "no CUDA device available");
+    if (device < 0 || device >= count) fail(kInvalidArgument, "device index out of range");
+    cudaDeviceProp prop;
+    DSG_CUDA_CHECK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) fail(kInvalidArgument, "libdsg is built for sm_100a (B200) only");
+    auto* c = new dsg_ctx_s();
+    c->device = device;
+    DeviceGuard g(device);
+    DSG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c;
+  });
+}
+
+int dsg_ctx_destroy(dsg_ctx ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    DeviceGuard g(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto e : ctx->events) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int dsg_ctx_synchronize(dsg_ctx ctx) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dsg_model_create(dsg_ctx ctx, dsg_model* out) {
+  return guarded([&] {
+    (void)ctx;
+    *out = new dsg_model_s();
+  });
+}
+
+int dsg_model_destroy(dsg_model model) {
+  return guarded([&] { delete model; });
+}
+
+int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t n,
+                     int64_t iteration, int32_t origin_partition) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    if (n < 0) fail(kInvalidArgument, "negative model size");
+    ModelDev& m = model->m;
+    m.reserve(std::max<int64_t>(n, 1));
+    m.n = n;
+    m.iteration = iteration;
+    m.origin_partition = origin_partition;
+    if (n > 0) {
+      double* st = ctx->stage_d.ensure(kParams * n);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(st, params, sizeof(double) * kParams * n, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+      k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
+    }
+    reset_optimizer(ctx, m);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t capacity,
+                       int64_t* n, int64_t* iteration, int32_t* origin_partition) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    if (n) *n = m.n;
+    if (iteration) *iteration = m.iteration;
+    if (origin_partition) *origin_partition = m.origin_partition;
+    if (!params || m.n == 0) return;
+    if (capacity < m.n) fail(kInvalidArgument, "output capacity too small");
+    double* st = ctx->stage_d.ensure(kParams * m.n);
+    k_planar_to_aos<<<nblk(m.n), 256, 0, ctx->stream>>>(m.params.get(), m.cap, m.n, kParams, st);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(params, st, sizeof(double) * kParams * m.n, cudaMemcpyDeviceToHost,
+                                   ctx->stream));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dsg_model_info(dsg_model model, int64_t* n, int64_t* iteration, int64_t* adam_step) {
+  return guarded([&] {
+    if (n) *n = model->m.n;
+    if (iteration) *iteration = model->m.iteration;
+    if (adam_step) *adam_step = model->m.adam_step;
+  });
+}
+
+int dsg_model_adam_state(dsg_ctx ctx, dsg_model model, double* mo, double* vo, int64_t* step) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    if (step) *step = m.adam_step;
+    if (m.n == 0) return;
+    double* st = ctx->stage_d.ensure(kParams * m.n);
+    for (int w = 0; w < 2; ++w) {
+      double* out = w == 0 ? mo : vo;
+      if (!out) continue;
+      k_planar_to_aos<<<nblk(m.n), 256, 0, ctx->stream>>>(w == 0 ? m.m.get() : m.v.get(), m.cap,
+                                                          m.n, kParams, st);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(out, st, sizeof(double) * kParams * m.n,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+  });
+}
+
+int dsg_render(dsg_ctx ctx, dsg_model model, const dsg_camera* cam_in,
+               const dsg_render_config* cfg, double* rgb, double* alpha, int32_t* n_contrib,
+               int32_t* splat_order, int64_t* n_order, int64_t* model_iteration) {
+  return guarded([&] {
+    RenderDev rd = make_rd(cfg);   // cfg.validate() first, like render.hpp:161
+    CamDev cam = make_cam(cam_in);
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    forward(ctx, m, cam, rd);
+    Frame& f = ctx->frame;
+    const int64_t npix = (int64_t)cam.width * cam.height;
+    cudaStream_t st = ctx->stream;
+    if (rgb || alpha) {
+      double* d = ctx->stage_d.ensure(4 * npix);
+      k_render_out<<<nblk(npix), 256, 0, st>>>(f.rgb.get(), f.T.get(), npix, d, d + 3 * npix);
+      if (rgb)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(rgb, d, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, st));
+      if (alpha)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(alpha, d + 3 * npix, sizeof(double) * npix,
+                                       cudaMemcpyDeviceToHost, st));
+    }
+    if (n_contrib)
+      DSG_CUDA_CHECK(cudaMemcpyAsync(n_contrib, f.ncontrib.get(), sizeof(int32_t) * npix,
+                                     cudaMemcpyDeviceToHost, st));
+    if (n_order) *n_order = f.n_visible;
+    if (splat_order && f.n_visible > 0)
+      DSG_CUDA_CHECK(cudaMemcpyAsync(splat_order, f.sorted_idx, sizeof(int32_t) * f.n_visible,
+                                     cudaMemcpyDeviceToHost, st));
+    if (model_iteration) *model_iteration = m.iteration;
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int dsg_bin(dsg_ctx ctx, dsg_model model, const dsg_camera* cam_in, const dsg_render_config* cfg,
+            int32_t* tile_count, int32_t* entries, int64_t capacity, int64_t* n_entries) {
+  return guarded([&] {
+    RenderDev rd = make_rd(cfg);
+    CamDev cam = make_cam(cam_in);
+    DeviceGuard g(ctx->device);
+    Frame& f = ctx->frame;
+    bin_frame(f, model->m.params.get(), model->m.cap, model->m.n, cam, rd, ctx->stream);
+    *n_entries = f.n_dup;
+    std::vector<uint2> ranges(f.tiles);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(ranges.data(), f.ranges.get(), sizeof(uint2) * f.tiles,
+                                   cudaMemcpyDeviceToHost, ctx->stream));
+    if (f.n_dup > capacity) fail(kInvalidArgument, "entry capacity too small");
+    if (f.n_dup > 0)
+      DSG_CUDA_CHECK(cudaMemcpyAsync(entries, f.sorted_val, sizeof(int32_t) * f.n_dup,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    for (int64_t t = 0; t < f.tiles; ++t) tile_count[t] = (int32_t)(ranges[t].y - ranges[t].x);
+  });
+}
+
+int dsg_masked_loss(dsg_ctx ctx, const double* rendered, const double* ground_truth,
+                    const double* mask, int32_t width, int32_t height, double loss_lambda,
+                    double* loss, double* dL_dpixels) {
+  return guarded([&] {
+    if (width <= 0 || height <= 0) fail(kDimensionMismatch, "image dimensions differ");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    Frame& f = ctx->frame;
+    const int64_t npix = (int64_t)width * height;
+    double* d = ctx->stage_d.ensure(7 * npix);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, rendered, sizeof(double) * 3 * npix, cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d + 3 * npix, ground_truth, sizeof(double) * 3 * npix,
+                                   cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d + 6 * npix, mask, sizeof(double) * npix, cudaMemcpyHostToDevice, st));
+    f.rgb.ensure(3 * npix);
+    float* gt = ctx->stage_f.ensure(3 * npix);
+    uint8_t* m8 = ctx->stage_u8.ensure(npix);
+    k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d, npix, 3, f.rgb.get(), npix);
+    k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d + 3 * npix, npix, 3, gt, npix);
+    k_mask_u8<<<nblk(npix), 256, 0, st>>>(d + 6 * npix, npix, m8);
+    masked_loss_dev(f, gt, m8, width, height, loss_lambda, st);
+    k_planar_to_aos<<<nblk(npix), 256, 0, st>>>(f.dL.get(), npix, npix, 3, d);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(dL_dpixels, d, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(loss, f.loss_out.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int dsg_backward(dsg_ctx ctx, dsg_model model, const dsg_camera* cam_in,
+                 const dsg_render_config* cfg, int64_t output_iteration,
+                 const double* dL_dpixels, int32_t shards, double* grads, double* d_mean2d,
+                 int32_t* touch_count) {
+  return guarded([&] {
+    ModelDev& m = model->m;
+    // checks in the order of backward.hpp:187-192
+    if (output_iteration != m.iteration)
+      fail(kStaleForward, "render output is from a different model iteration");
+    if (!cam_in || !dL_dpixels) fail(kDimensionMismatch, "dL_dpixels must be RGB at camera resolution");
+    if (shards < 1) fail(kInvalidArgument, "shards must be >= 1");
+    RenderDev rd = make_rd(cfg);
+    CamDev cam = make_cam(cam_in);
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    Frame& f = ctx->frame;
+    const int64_t npix = (int64_t)cam.width * cam.height;
+    forward(ctx, m, cam, rd);
+    double* d = ctx->stage_d.ensure(std::max<int64_t>(3 * npix, kParams * std::max<int64_t>(m.n, 1)));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, dL_dpixels, sizeof(double) * 3 * npix, cudaMemcpyHostToDevice, st));
+    f.dL.ensure(3 * npix);
+    k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d, npix, 3, f.dL.get(), npix);
+    backward_dev(ctx, m, cam, rd);
+    if (m.n > 0) {
+      if (grads) {
+        k_planar_to_aos<<<nblk(m.n), 256, 0, st>>>(m.grads.get(), m.cap, m.n, kParams, d);
+        DSG_CUDA_CHECK(cudaMemcpyAsync(grads, d, sizeof(double) * kParams * m.n, cudaMemcpyDeviceToHost, st));
+        DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+      }
+      if (d_mean2d) {
+        k_planar_to_aos<<<nblk(m.n), 256, 0, st>>>(m.dmean.get(), m.cap, m.n, 2, d);
+        DSG_CUDA_CHECK(cudaMemcpyAsync(d_mean2d, d, sizeof(double) * 2 * m.n, cudaMemcpyDeviceToHost, st));
+        DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+      }
+      if (touch_count)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(touch_count, m.touch.get(), sizeof(int32_t) * m.n,
+                                       cudaMemcpyDeviceToHost, st));
+    }
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int dsg_adam_step(dsg_ctx ctx, dsg_model model, const double* grads, const dsg_group_rates* rates,
+                  const dsg_adam_config* adam) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    cudaStream_t st = ctx->stream;
+    m.adam_step += 1;
+    if (m.n == 0) return;
+    double* d = ctx->stage_d.ensure(kParams * m.n);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, grads, sizeof(double) * kParams * m.n, cudaMemcpyHostToDevice, st));
+    k_aos_to_planar<<<nblk(m.n), 256, 0, st>>>(d, m.n, kParams, m.grads.get(), m.cap);
+    double r[5] = {rates->mu, rates->log_scale, rates->rot, rates->opacity, rates->color};
+    adam_update(make_adam(m, r, *adam, m.adam_step, false), st);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int dsg_views_create(dsg_ctx ctx, const dsg_camera* cams, const double* ground_truth,
+                     const double* masks, int32_t n_views, dsg_views* out) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    auto* v = new dsg_views_s();
+    try {
+      v->n = n_views;
+      if (n_views > 0) {
+        v->width = cams[0].width;
+        v->height = cams[0].height;
+        for (int32_t i = 0; i < n_views; ++i) {
+          make_cam(&cams[i]);
+          if (cams[i].width != v->width || cams[i].height != v->height)
+            fail(kDimensionMismatch, "all views must share one resolution");
+          v->cams.push_back(cams[i]);
+        }
+        const int64_t npix = (int64_t)v->width * v->height;
+        v->gt.ensure(3 * npix * n_views);
+        v->mask.ensure(npix * n_views);
+        double* d = ctx->stage_d.ensure(4 * npix);
+        for (int32_t i = 0; i < n_views; ++i) {
+          DSG_CUDA_CHECK(cudaMemcpyAsync(d, ground_truth + 3 * npix * i, sizeof(double) * 3 * npix,
+                                         cudaMemcpyHostToDevice, ctx->stream));
+          DSG_CUDA_CHECK(cudaMemcpyAsync(d + 3 * npix, masks + npix * i, sizeof(double) * npix,
+                                         cudaMemcpyHostToDevice, ctx->stream));
+          k_aos_to_planar<<<nblk(npix), 256, 0, ctx->stream>>>(d, npix, 3, v->gt.get() + 3 * npix * i, npix);
+          k_mask_u8<<<nblk(npix), 256, 0, ctx->stream>>>(d + 3 * npix, npix, v->mask.get() + npix * i);
+        }
+        DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      }
+    } catch (...) {
+      delete v;
+      throw;
+    }
+    *out = v;
+  });
+}
+
+int dsg_views_destroy(dsg_views views) {
+  return guarded([&] { delete views; });
+}
+
+int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t i, double* ground_truth,
+                       double* mask) {
+  return guarded([&] {
+    if (i < 0 || i >= views->n) fail(kInvalidArgument, "view index out of range");
+    DeviceGuard g(ctx->device);
+    const int64_t npix = (int64_t)views->width * views->height;
+    double* d = ctx->stage_d.ensure(3 * npix);
+    if (ground_truth) {
+      k_planar_to_aos<<<nblk(npix), 256, 0, ctx->stream>>>(views->gt.get() + 3 * npix * i, npix,
+                                                           npix, 3, d);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(ground_truth, d, sizeof(double) * 3 * npix,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    }
+    if (mask) {
+      std::vector<uint8_t> m8(npix);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(m8.data(), views->mask.get() + npix * i, npix,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+      for (int64_t k = 0; k < npix; ++k) mask[k] = m8[k] ? 1.0 : 0.0;
+    }
+  });
+}
+
+int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_config* cfg,
+              int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
+              double* loss_trace) {
+  return guarded([&] {
+    validate_train(cfg);
+    if (!views || views->n <= 0) fail(kNoViews, "training requires at least one view");
+    if (shards < 1) fail(kInvalidArgument, "shards must be >= 1");
+    if (final_loss) *final_loss = 0.0;
+    ModelDev& m = model->m;
+    if (cfg->iterations == 0) return;
+    const int64_t iters = cfg->iterations;
+    const int64_t until = (int64_t)(cfg->densify_stop_fraction * (double)iters);
+    if (cfg->densify_interval > 0)
+      for (int64_t it = 0; it < iters; ++it)
+        if ((it + 1) % cfg->densify_interval == 0 && (it + 1) < until)
+          fail(kInvalidArgument, "densification is not yet implemented on the device");
+    RenderDev rd = make_rd(&cfg->render);
+    std::vector<CamDev> cams;
+    for (const auto& c : views->cams) cams.push_back(make_cam(&c));
+    // seeded view order (trainer.hpp:157-163)
+    std::vector<size_t> order(views->n);
+    std::iota(order.begin(), order.end(), size_t{0});
+    Rng vr(cfg->seed ^ 0x87aa11d3ULL);
+    for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[(size_t)vr.below(i)]);
+
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    reset_optimizer(ctx, m);   // fresh AdamState and stats (trainer.hpp:167-168)
+    const int64_t npix = (int64_t)views->width * views->height;
+    double* trace = ctx->loss_trace.ensure(iters);
+    const bool prof = ctx->profile;
+    if (ctx->events.size() < 8) {
+      for (size_t k = ctx->events.size(); k < 8; ++k) {
+        cudaEvent_t e;
+        DSG_CUDA_CHECK(cudaEventCreate(&e));
+        ctx->events.push_back(e);
+      }
+    }
+    double stage[6] = {0, 0, 0, 0, 0, 0};
+    DSG_CUDA_CHECK(cudaEventRecord(ctx->events[7], st));
+    for (int64_t it = 0; it < iters; ++it) {
+      const size_t vi = order[(size_t)it % order.size()];
+      const CamDev& cam = cams[vi];
+      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[0], st));
+      bin_frame(ctx->frame, m.params.get(), m.cap, m.n, cam, rd, st);
+      Frame& f = ctx->frame;
+      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[1], st));
+      if (f.n_visible == 0 || f.n_dup == 0) {
+        forward(ctx, m, cam, rd);
+      } else {
+        blend_forward(f, m.params.get(), m.cap, cam, rd, st);
+      }
+      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[2], st));
+      masked_loss_dev(f, views->gt.get() + 3 * npix * vi, views->mask.get() + npix * vi,
+                      views->width, views->height, cfg->loss_lambda, st);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(trace + it, f.loss_out.get(), sizeof(double),
+                                     cudaMemcpyDeviceToDevice, st));
+      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[3], st));
+      if (f.n_visible > 0 && f.n_dup > 0) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
+      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[4], st));
+      {
+        if (f.n_visible == 0 || f.n_dup == 0) {
+          DSG_CUDA_CHECK(cudaMemsetAsync(m.grads.get(), 0, sizeof(float) * kParams * m.cap, st));
+          DSG_CUDA_CHECK(cudaMemsetAsync(m.touch.get(), 0, sizeof(int32_t) * m.cap, st));
+          DSG_CUDA_CHECK(cudaMemsetAsync(m.dmean.get(), 0, sizeof(float) * 2 * m.cap, st));
+        } else {
+          ChainArgs a;
+          a.params = m.params.get();
+          a.pitch = m.cap;
+          a.n = m.n;
+          a.cam = cam;
+          a.tcount = f.tcount.get();
+          a.dup_base = f.dup_base.get();
+          a.partials = f.partials.get();
+          a.grads = m.grads.get();
+          a.dmean = m.dmean.get();
+          a.touch = m.touch.get();
+          chain_3d(a, st);
+        }
+      }
+      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[5], st));
+      const double decay = std::pow(cfg->lr_mu_decay, (double)it / (double)iters);
+      const double rates[5] = {cfg->lr_mu * decay, cfg->lr_scale, cfg->lr_rot, cfg->lr_opacity,
+                               cfg->lr_color};
+      m.adam_step += 1;
+      adam_update(make_adam(m, rates, cfg->adam, m.adam_step, true), st);
+      m.iteration += 1;
+      if (prof) {
+        DSG_CUDA_CHECK(cudaEventRecord(ctx->events[6], st));
+        DSG_CUDA_CHECK(cudaEventSynchronize(ctx->events[6]));
+        float ms;
+        for (int s = 0; s < 6; ++s) {
+          DSG_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->events[s], ctx->events[s + 1]));
+          stage[s] += ms;
+        }
+      }
+      if (progress) {
+        double l;
+        DSG_CUDA_CHECK(cudaMemcpyAsync(&l, trace + it, sizeof(double), cudaMemcpyDeviceToHost, st));
+        DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+        progress(it + 1, l, user);
+      }
+    }
+    DSG_CUDA_CHECK(cudaEventRecord(ctx->events[6], st));
+    DSG_CUDA_CHECK(cudaEventSynchronize(ctx->events[6]));
+    float total;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&total, ctx->events[7], ctx->events[6]));
+    ctx->last_total_ms = total;
+    for (int s = 0; s < 6; ++s) ctx->last_stage_ms[s] = stage[s];
+    std::vector<double> tr(iters);
+    DSG_CUDA_CHECK(cudaMemcpy(tr.data(), trace, sizeof(double) * iters, cudaMemcpyDeviceToHost));
+    if (final_loss) *final_loss = tr.back();
+    if (loss_trace) std::memcpy(loss_trace, tr.data(), sizeof(double) * iters);
+  });
+}
+
+int dsg_set_profiling(dsg_ctx ctx, int32_t enable) {
+  return guarded([&] { ctx->profile = enable != 0; });
+}
+
+int dsg_render_mask(dsg_ctx ctx, const double* points, int64_t n, const dsg_camera* cam_in,
+                    double footprint_px, double dilation_px, double* mask) {
+  return guarded([&] {
+    // render.hpp:212-214: footprint check, then camera validation
+    if (footprint_px < 0.5) fail(kInvalidArgument, "footprint_px must be >= 0.5");
+    CamDev cam = make_cam(cam_in);
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t npix = (int64_t)cam.width * cam.height;
+    uint8_t* m8 = ctx->stage_u8.ensure(npix);
+    DSG_CUDA_CHECK(cudaMemsetAsync(m8, 0, npix, st));
+    if (n > 0) {
+      double* d = ctx->stage_d2.ensure(3 * n);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(d, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+      render_mask_dev(d, n, cam, footprint_px + dilation_px, m8, st);
+    }
+    std::vector<uint8_t> h(npix);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), m8, npix, cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < npix; ++i) mask[i] = h[i] ? 1.0 : 0.0;
+  });
+}
+
+int dsg_views_synthesize(dsg_ctx ctx, dsg_model gt_model, const dsg_render_config* cfg,
+                         const dsg_camera* cams, int32_t n_views, const double* points,
+                         int64_t n_points, int32_t use_masks, double footprint_px,
+                         double dilation_px, dsg_views* out) {
+  return guarded([&] {
+    RenderDev rd = make_rd(cfg);
+    if (use_masks && footprint_px < 0.5) fail(kInvalidArgument, "footprint_px must be >= 0.5");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    auto* v = new dsg_views_s();
+    try {
+      v->n = n_views;
+      if (n_views > 0) {
+        v->width = cams[0].width;
+        v->height = cams[0].height;
+      }
+      const int64_t npix = (int64_t)v->width * v->height;
+      v->gt.ensure(std::max<int64_t>(1, 3 * npix * n_views));
+      v->mask.ensure(std::max<int64_t>(1, npix * n_views));
+      double* dpts = nullptr;
+      if (use_masks && n_points > 0) {
+        dpts = ctx->stage_d2.ensure(3 * n_points);
+        DSG_CUDA_CHECK(cudaMemcpyAsync(dpts, points, sizeof(double) * 3 * n_points,
+                                       cudaMemcpyHostToDevice, st));
+      }
+      for (int32_t i = 0; i < n_views; ++i) {
+        CamDev cam = make_cam(&cams[i]);
+        if (cams[i].width != v->width || cams[i].height != v->height)
+          fail(kDimensionMismatch, "all views must share one resolution");
+        v->cams.push_back(cams[i]);
+        forward(ctx, gt_model->m, cam, rd);  // ground truth = render(gt_model) (runtime.hpp:195)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(v->gt.get() + 3 * npix * i, ctx->frame.rgb.get(),
+                                       sizeof(float) * 3 * npix, cudaMemcpyDeviceToDevice, st));
+        uint8_t* mi = v->mask.get() + npix * i;
+        if (use_masks) {
+          DSG_CUDA_CHECK(cudaMemsetAsync(mi, 0, npix, st));
+          if (n_points > 0) render_mask_dev(dpts, n_points, cam, footprint_px + dilation_px, mi, st);
+        } else {
+          DSG_CUDA_CHECK(cudaMemsetAsync(mi, 1, npix, st));
+        }
+      }
+      DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    } catch (...) {
+      delete v;
+      throw;
+    }
+    *out = v;
+  });
+}
+
+int dsg_last_timing(dsg_ctx ctx, double* total_ms, double* stage_ms) {
+  return guarded([&] {
+    if (total_ms) *total_ms = ctx->last_total_ms;
+    if (stage_ms)
+      for (int s = 0; s < 6; ++s) stage_ms[s] = ctx->last_stage_ms[s];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,217 @@
+// K1 preprocess, depth-sort fix-up, K2 duplicate, K4 tile ranges (sm_100a).
+//
+// K1 replaces try_project (projection.hpp:24-57) and the cull/rect part of
+// prepare_splats (render.hpp:62-97). Every integer- or order-producing value
+// (camera-space depth, mean2d, cov2d, pixel rect, culling) is computed in
+// exact fp64 without FMA contraction, so rects, tile counts and the sorted
+// key lists match the x86-64 reference bit-for-bit; the blend payload is
+// stored as fp32 (mean2d as a hi/lo pair so pixel offsets stay exact).
+//
+// Ordering: visible splats are sorted by fp32 depth bits (monotone in the
+// fp64 depth), runs of equal fp32 keys are re-ordered by (fp64 depth, index)
+// — the reference comparator (render.hpp:98-101) — and the duplicates are
+// then stably sorted by tile id, so every tile list is in reference
+// compositing order.
+#include "dsg_internal.h"
+#include "raster.h"
+#include "scan_util.cuh"
+
+namespace dsg {
+
+namespace {
+
+__global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  bool vis = false;
+  float depth_f = 0.f;
+  if (i < a.n) {
+    double p[kParams];
+#pragma unroll
+    for (int k = 0; k < kParams; ++k) p[k] = (double)a.params[(int64_t)k * a.pitch + i];
+    Proj64 pr;
+    uint32_t count = 0;
+    if (project64(p, a.cam, pr)) {
+      double rx = dm(a.rd.sigma_cutoff, sqrt(pr.cxx));
+      double ry = dm(a.rd.sigma_cutoff, sqrt(pr.cyy));
+      int x0 = max(to_int_x86(ceil(ds(ds(pr.mx, rx), 0.5))), 0);
+      int x1 = min(to_int_x86(floor(ds(da(pr.mx, rx), 0.5))), a.cam.width - 1);
+      int y0 = max(to_int_x86(ceil(ds(ds(pr.my, ry), 0.5))), 0);
+      int y1 = min(to_int_x86(floor(ds(da(pr.my, ry), 0.5))), a.cam.height - 1);
+      double det = ds(dm(pr.cxx, pr.cyy), dm(pr.cxy, pr.cxy));
+      if (x0 <= x1 && y0 <= y1 && det > 0.0) {
+        double ixx = dd(pr.cyy, det), ixy = dd(-pr.cxy, det), iyy = dd(pr.cxx, det);
+        double op = sigmoid64(p[10]);
+        // conditioning of the conic: bounds the fp32 rounding of q (guard band)
+        double tr = ixx + iyy, df = ixx - iyy;
+        double lmax = 0.5 * (tr + sqrt(df * df + 4.0 * ixy * ixy));
+        double lmin = (1.0 / det) / lmax;
+        double kappa = (fabs(ixx) + fabs(iyy) + 2.0 * fabs(ixy)) / lmin;
+        float mxh = (float)pr.mx, myh = (float)pr.my;
+        float4* r = a.rec + 3 * i;
+        r[0] = make_float4(mxh, myh, (float)(pr.mx - (double)mxh), (float)(pr.my - (double)myh));
+        r[1] = make_float4((float)ixx, (float)ixy, (float)iyy, (float)op);
+        r[2] = make_float4((float)p[11], (float)p[12], (float)p[13], (float)kappa);
+        int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
+        a.trect[i] = make_int4(tx0, ty0, tx1, ty1);
+        count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+        a.depth[i] = pr.depth;
+        depth_f = (float)pr.depth;
+        vis = true;
+      }
+    }
+    a.tcount[i] = count;
+  }
+  // warp-aggregated compaction of the visible set (order fixed by the sort)
+  uint32_t mask = __ballot_sync(0xffffffffu, vis);
+  if (mask == 0) return;
+  uint32_t base = 0;
+  if (lane == __ffs(mask) - 1) base = atomicAdd(a.vis_count, (uint32_t)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+  if (vis) {
+    uint32_t slot = base + __popc(mask & ((1u << lane) - 1u));
+    a.vis_key[slot] = __float_as_uint(depth_f);
+    a.vis_idx[slot] = (uint32_t)i;
+  }
+}
+
+// Re-order runs of equal fp32 depth keys by (fp64 depth, index): the
+// reference comparator (render.hpp:98-101). Runs are tiny; insertion sort.
+__global__ void k_depth_fixup(const uint32_t* __restrict__ key, uint32_t* idx, int64_t n,
+                              const double* __restrict__ depth) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n) return;
+  uint32_t k = key[s];
+  if (s > 0 && key[s - 1] == k) return;          // not a run start
+  if (s + 1 >= n || key[s + 1] != k) return;     // singleton
+  int64_t e = s + 1;
+  while (e < n && key[e] == k) ++e;
+  for (int64_t j = s + 1; j < e; ++j) {
+    uint32_t v = idx[j];
+    double dv = depth[v];
+    int64_t m = j - 1;
+    while (m >= s) {
+      uint32_t u = idx[m];
+      double du = depth[u];
+      if (du < dv || (du == dv && u < v)) break;
+      idx[m + 1] = u;
+      --m;
+    }
+    idx[m + 1] = v;
+  }
+}
+
+__global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv,
+                                const uint32_t* __restrict__ tcount, uint32_t* out) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nv) out[s] = tcount[vis_idx[s]];
+}
+
+// K2: one (tile id, gaussian index) pair per overlapped tile, emitted in
+// depth order; tile enumeration row-major inside the rect (render.hpp:127-133).
+__global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
+                            const uint32_t* __restrict__ offs, const int4* __restrict__ trect,
+                            int tiles_x, uint32_t* __restrict__ tile_key,
+                            uint32_t* __restrict__ dup_val, uint32_t* __restrict__ dup_base) {
+  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nv) return;
+  uint32_t i = vis_idx[s];
+  uint32_t o = offs[s];
+  dup_base[i] = o;
+  int4 r = trect[i];
+  for (int ty = r.y; ty <= r.w; ++ty)
+    for (int tx = r.x; tx <= r.z; ++tx) {
+      tile_key[o] = (uint32_t)(ty * tiles_x + tx);
+      dup_val[o] = i;
+      ++o;
+    }
+}
+
+// K4: [start, end) of every tile in the sorted duplicate list.
+__global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd, uint2* ranges) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nd) return;
+  uint32_t t = tile_key[e];
+  if (e == 0 || tile_key[e - 1] != t) ranges[t].x = (uint32_t)e;
+  if (e == nd - 1 || tile_key[e + 1] != t) ranges[t].y = (uint32_t)(e + 1);
+}
+
+inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
+               const RenderDev& rd, cudaStream_t st) {
+  f.n = n;
+  f.tiles = (int64_t)cam.tiles_x * cam.tiles_y;
+  f.rec.ensure(3 * (size_t)std::max<int64_t>(n, 1));
+  f.trect.ensure(std::max<int64_t>(n, 1));
+  f.tcount.ensure(std::max<int64_t>(n, 1));
+  f.depth.ensure(std::max<int64_t>(n, 1));
+  f.dup_base.ensure(std::max<int64_t>(n, 1));
+  f.vis_key.ensure(std::max<int64_t>(n, 1));
+  f.vis_idx.ensure(std::max<int64_t>(n, 1));
+  f.vis_key2.ensure(std::max<int64_t>(n, 1));
+  f.vis_idx2.ensure(std::max<int64_t>(n, 1));
+  f.offs.ensure(std::max<int64_t>(n, 1) + 1);
+  f.ranges.ensure(f.tiles);
+  f.counters.ensure(4);
+  DSG_CUDA_CHECK(cudaMemsetAsync(f.counters.get(), 0, 4 * sizeof(uint32_t), st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(f.ranges.get(), 0, f.tiles * sizeof(uint2), st));
+  f.n_visible = 0;
+  f.n_dup = 0;
+  if (n > 0) {
+    PreprocessArgs a;
+    a.params = params;
+    a.pitch = pitch;
+    a.n = n;
+    a.cam = cam;
+    a.rd = rd;
+    a.rec = f.rec.get();
+    a.trect = f.trect.get();
+    a.tcount = f.tcount.get();
+    a.depth = f.depth.get();
+    a.vis_key = f.vis_key.get();
+    a.vis_idx = f.vis_idx.get();
+    a.vis_count = f.counters.get();
+    k_preprocess<<<blocks(n, 256), 256, 0, st>>>(a);
+    DSG_CUDA_CHECK(cudaGetLastError());
+    uint32_t nv = 0;
+    DSG_CUDA_CHECK(cudaMemcpyAsync(&nv, f.counters.get(), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    f.n_visible = nv;
+  }
+  const int64_t nv = f.n_visible;
+  if (nv == 0) return;
+  // depth sort of the visible set (stable; key = fp32 depth bits)
+  bool alt = radix_sort_pairs<uint32_t>(f.vis_key.get(), f.vis_idx.get(), f.vis_key2.get(),
+                                         f.vis_idx2.get(), nv, 0, 32, f.sort, st);
+  uint32_t* skey = alt ? f.vis_key2.get() : f.vis_key.get();
+  uint32_t* sidx = alt ? f.vis_idx2.get() : f.vis_idx.get();
+  k_depth_fixup<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get());
+  f.sorted_idx = sidx;
+  // per-splat tile counts in depth order, exclusive scan -> duplicate slots
+  uint32_t* cnt = alt ? f.vis_key.get() : f.vis_key2.get();  // free buffer
+  k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+  exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
+  uint32_t nd = 0;
+  DSG_CUDA_CHECK(cudaMemcpyAsync(&nd, f.offs.get() + nv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  f.n_dup = nd;
+  f.tile_key.ensure(std::max<uint32_t>(nd, 1));
+  f.dup_val.ensure(std::max<uint32_t>(nd, 1));
+  f.tile_key2.ensure(std::max<uint32_t>(nd, 1));
+  f.dup_val2.ensure(std::max<uint32_t>(nd, 1));
+  k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(), cam.tiles_x,
+                                               f.tile_key.get(), f.dup_val.get(), f.dup_base.get());
+  int tile_bits = 1;
+  while ((int64_t(1) << tile_bits) < f.tiles) ++tile_bits;
+  bool alt2 = radix_sort_pairs<uint32_t>(f.tile_key.get(), f.dup_val.get(), f.tile_key2.get(),
+                                          f.dup_val2.get(), nd, 0, tile_bits, f.sort, st);
+  f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
+  f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
+  k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get());
+  DSG_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace dsg

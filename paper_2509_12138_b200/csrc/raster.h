@@ -1,0 +1,109 @@
+// Raster pipeline state for one view (per context scratch) and launchers.
+#pragma once
+#include "dsg_internal.h"
+
+namespace dsg {
+
+struct PreprocessArgs {
+  const float* params;  // [14][pitch] planar fp32 model
+  int64_t pitch, n;
+  CamDev cam;
+  RenderDev rd;
+  float4* rec;          // [n][3] blend payload (model order)
+  int4* trect;          // [n] tile rect (tx0, ty0, tx1, ty1)
+  uint32_t* tcount;     // [n] overlapped tiles (0 = culled)
+  double* depth;        // [n] camera-space depth (fp64)
+  uint32_t* vis_key;    // [n] compacted fp32 depth bits
+  uint32_t* vis_idx;    // [n] compacted gaussian index
+  uint32_t* vis_count;
+};
+
+// Scratch for one rendered view: binning products, per-pixel forward state,
+// loss buffers and backward partials.
+struct Frame {
+  int64_t n = 0, n_visible = 0, n_dup = 0, tiles = 0;
+  int width = 0, height = 0;
+  // per gaussian (model order)
+  DevBuf<float4> rec;
+  DevBuf<int4> trect;
+  DevBuf<uint32_t> tcount, dup_base;
+  DevBuf<double> depth;
+  // visible set, depth-sorted
+  DevBuf<uint32_t> vis_key, vis_idx, vis_key2, vis_idx2, offs;
+  uint32_t* sorted_idx = nullptr;
+  // duplicates
+  DevBuf<uint32_t> tile_key, dup_val, tile_key2, dup_val2;
+  uint32_t* sorted_tile = nullptr;
+  uint32_t* sorted_val = nullptr;
+  DevBuf<uint2> ranges;
+  DevBuf<uint32_t> counters;
+  // per pixel (planar fp32)
+  DevBuf<float> rgb, T, dL;
+  DevBuf<uint32_t> last;
+  DevBuf<int32_t> ncontrib;
+  // backward partials [n_dup][10]
+  DevBuf<float> partials;
+  // loss scratch
+  DevBuf<double> ssim_pqr, loss_parts;
+  DevBuf<uint32_t> loss_counts;
+  DevBuf<double> loss_out;
+  SortScratch sort;
+  ScanScratch scan;
+};
+
+// Model tensors on device (planar [14][cap] fp32 for params/grads/moments).
+struct ModelDev {
+  int64_t n = 0, cap = 0;
+  int64_t iteration = 0;
+  int32_t origin_partition = -1;
+  int64_t adam_step = 0;
+  DevBuf<float> params, grads, m, v, dmean, stat_norm;
+  DevBuf<int32_t> touch, stat_count;
+  void reserve(int64_t c);
+};
+
+struct ChainArgs {
+  const float* params;
+  int64_t pitch, n;
+  CamDev cam;
+  const uint32_t* tcount;
+  const uint32_t* dup_base;
+  const float* partials;
+  float* grads;     // [14][pitch]
+  float* dmean;     // [2][pitch]
+  int32_t* touch;   // [n]
+};
+
+struct AdamArgs {
+  float* params;
+  const float* grads;
+  float* m;
+  float* v;
+  const float* dmean;
+  const int32_t* touch;
+  float* stat_norm;
+  int32_t* stat_count;
+  int64_t pitch, n;
+  float lr[5];
+  float b1, b2, omb1, omb2, inv_bc1, inv_bc2, eps;
+  float ls_lo, ls_hi;
+  int accumulate_stats;
+};
+
+void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
+               const RenderDev& rd, cudaStream_t st);
+void blend_forward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,
+                   const RenderDev& rd, cudaStream_t st);
+void blend_backward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,
+                    const RenderDev& rd, cudaStream_t st);
+void chain_3d(const ChainArgs& a, cudaStream_t st);
+void adam_update(const AdamArgs& a, cudaStream_t st);
+// Masked L1 + D-SSIM on f.rgb vs (gt, mask); writes f.dL and the loss into
+// f.loss_out[0] (device). gt planar fp32 [3][h*w], mask u8 [h*w].
+// K11: stamp render_mask discs of `radius` px into a zeroed byte mask.
+void render_mask_dev(const double* pts, int64_t n, const CamDev& cam, double radius,
+                     uint8_t* mask, cudaStream_t st);
+void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
+                     double lambda, cudaStream_t st);
+
+}  // namespace dsg

@@ -1,0 +1,309 @@
+// Onesweep LSD radix sort and exclusive scan (sm_100a).
+//
+// Replaces the reference's std::sort by (depth, index) (render.hpp:98-101)
+// and the std::vector push_back binning (render.hpp:117-135): the raster
+// pipeline sorts visible splats by depth once, duplicates them per tile in
+// that order, then sorts the duplicates stably by tile id with this kernel,
+// which reproduces the reference's per-tile compositing order exactly.
+//
+// Per digit pass: each CTA takes a ticket (partition id), loads 256x12 keys
+// warp-striped (coalesced), ranks them per digit with warp match/popc in input
+// order (stable), publishes its digit counts with a 2-bit flag in one 32-bit
+// word, looks back over earlier partitions to form its exclusive digit
+// prefix, stages the keys digit-sorted in shared memory and writes them out
+// in coalesced runs. The global digit bases come from one histogram pass.
+#include "dsg_internal.h"
+#include "scan_util.cuh"
+
+namespace dsg {
+
+namespace {
+
+constexpr int kRadixBits = 8;
+constexpr int kRadix = 256;
+constexpr int kSortThreads = 256;
+constexpr int kSortWarps = kSortThreads / 32;
+constexpr int kSortItems = 12;
+constexpr int kPart = kSortThreads * kSortItems;  // keys per partition
+constexpr uint32_t kFlagAgg = 1u << 30;
+constexpr uint32_t kFlagPrefix = 2u << 30;
+constexpr uint32_t kValueMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+template <class K>
+__global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, int64_t n,
+                                                    int begin_bit, int passes,
+                                                    uint32_t* __restrict__ ghist) {
+  __shared__ uint32_t h[8][kRadix];
+  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    bool valid = i < n;
+    K k = valid ? keys[i] : K(0);
+    for (int p = 0; p < passes; ++p) {
+      uint32_t d = valid ? (uint32_t)((k >> (begin_bit + kRadixBits * p)) & (kRadix - 1)) : 0x100u;
+      // warp-aggregated increment: keys are often clustered in one digit
+      uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&h[p][d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
+    uint32_t v = (&h[0][0])[i];
+    if (v) atomicAdd(&ghist[i], v);
+  }
+}
+
+// Exclusive scan of each pass's 256 bins (one block per pass).
+__global__ void k_hist_scan(uint32_t* ghist) {
+  __shared__ uint32_t tmp[32];
+  uint32_t* h = ghist + blockIdx.x * kRadix;
+  uint32_t agg;
+  uint32_t ex = block_exclusive_sum<kRadix>(h[threadIdx.x], &agg, tmp);
+  h[threadIdx.x] = ex;
+}
+
+template <class K>
+struct OnesweepSmem {
+  uint32_t warp_hist[kSortWarps][kRadix];
+  uint32_t block_excl[kRadix];
+  uint32_t global_base[kRadix];
+  K keys[kPart];
+  uint32_t vals[kPart];
+  uint32_t part;
+  uint32_t scan[32];
+};
+
+template <class K>
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ gscan,
+    uint32_t* status, uint32_t* counter) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  OnesweepSmem<K>& sm = *reinterpret_cast<OnesweepSmem<K>*>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) sm.part = atomicAdd(counter, 1u);
+  for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t part = sm.part;
+  const int64_t base = (int64_t)part * kPart;
+
+  K k[kSortItems];
+  uint32_t v[kSortItems];
+  uint32_t dig[kSortItems];
+  uint32_t rank[kSortItems];
+  const int64_t wbase = base + (int64_t)warp * 32 * kSortItems;
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    int64_t idx = wbase + i * 32 + lane;
+    bool valid = idx < n;
+    k[i] = valid ? kin[idx] : K(0);
+    v[i] = valid ? vin[idx] : 0u;
+    dig[i] = valid ? (uint32_t)((k[i] >> shift) & (kRadix - 1)) : 0x100u;
+  }
+  const uint32_t lt = lanemask_lt();
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    uint32_t d = dig[i];
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    uint32_t before = d < kRadix ? sm.warp_hist[warp][d] : 0u;
+    __syncwarp();
+    if (d < kRadix && (__ffs(peers) - 1) == lane) sm.warp_hist[warp][d] = before + __popc(peers);
+    __syncwarp();
+    rank[i] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+
+  // Thread d owns digit d: exclusive offsets across warps, block total.
+  const int d = tid;
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < kSortWarps; ++w) {
+    uint32_t c = sm.warp_hist[w][d];
+    sm.warp_hist[w][d] = total;
+    total += c;
+  }
+  // Decoupled look-back over earlier partitions for this digit.
+  volatile uint32_t* vs = status;
+  uint32_t excl = 0;
+  if (part == 0) {
+    vs[d] = kFlagPrefix | total;
+  } else {
+    vs[(size_t)part * kRadix + d] = kFlagAgg | total;
+    int64_t p = (int64_t)part - 1;
+    while (true) {
+      uint32_t s = vs[(size_t)p * kRadix + d];
+      uint32_t flag = s & ~kValueMask;
+      if (flag == 0) continue;
+      excl += s & kValueMask;
+      if (flag == kFlagPrefix) break;
+      --p;
+    }
+    vs[(size_t)part * kRadix + d] = kFlagPrefix | (excl + total);
+  }
+  sm.global_base[d] = gscan[d] + excl;
+  uint32_t bagg;
+  uint32_t bex = block_exclusive_sum<kSortThreads>(total, &bagg, sm.scan);
+  sm.block_excl[d] = bex;
+  __syncthreads();
+
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    uint32_t dg = dig[i];
+    if (dg < kRadix) {
+      uint32_t pos = sm.block_excl[dg] + sm.warp_hist[warp][dg] + rank[i];
+      sm.keys[pos] = k[i];
+      sm.vals[pos] = v[i];
+    }
+  }
+  __syncthreads();
+  const int64_t remain = n - base;
+  const int count = remain < kPart ? (int)remain : kPart;
+  for (int j = tid; j < count; j += kSortThreads) {
+    K key = sm.keys[j];
+    uint32_t dg = (uint32_t)((key >> shift) & (kRadix - 1));
+    uint32_t out = sm.global_base[dg] + (uint32_t)j - sm.block_excl[dg];
+    kout[out] = key;
+    vout[out] = sm.vals[j];
+  }
+}
+
+// ---- exclusive scan (reduce, scan block sums, downsweep) ---------------------
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in,
+                                                              int64_t n, uint32_t* sums) {
+  __shared__ uint32_t tmp[32];
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (idx < n) s += in[idx];
+  }
+  uint32_t agg;
+  block_exclusive_sum<kScanThreads>(s, &agg, tmp);
+  s = agg;
+  if (threadIdx.x == 0) sums[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, int64_t nb) {
+  __shared__ uint32_t tmp[32];
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += 1024) {
+    int64_t i = base + threadIdx.x;
+    uint32_t v = i < nb ? sums[i] : 0u, agg;
+    uint32_t ex = block_exclusive_sum<1024>(v, &agg, tmp);
+    if (i < nb) sums[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[nb] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __restrict__ in,
+                                                            uint32_t* out, int64_t n,
+                                                            const uint32_t* __restrict__ sums) {
+  __shared__ uint32_t tmp[32];
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  uint32_t local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0u;
+    local += v[i];
+  }
+  uint32_t agg;
+  uint32_t run = block_exclusive_sum<kScanThreads>(local, &agg, tmp);
+  uint32_t ex[kScanItems];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    ex[i] = run;
+    run += v[i];
+  }
+  uint32_t off = sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i)
+    if (base + i < n) out[base + i] = ex[i] + off;
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
+}
+
+}  // namespace
+
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratch& s,
+                        cudaStream_t st) {
+  if (n <= 0) {
+    DSG_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(uint32_t), st));
+    return;
+  }
+  int64_t nb = (n + kScanTile - 1) / kScanTile;
+  uint32_t* sums = s.block_sums.ensure(nb + 1);
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
+  k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums);
+  DSG_CUDA_CHECK(cudaGetLastError());
+}
+
+template <class K>
+bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
+                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st) {
+  if (n <= 1 || end_bit <= begin_bit) return false;
+  if (n > (int64_t)kValueMask) fail(kInvalidArgument, "radix sort: too many keys");
+  const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
+  const int64_t parts = (n + kPart - 1) / kPart;
+  uint32_t* hist = s.hist.ensure((size_t)passes * kRadix);
+  uint32_t* status = s.status.ensure((size_t)passes * parts * kRadix);
+  uint32_t* counters = s.counters.ensure(passes);
+  DSG_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * passes * kRadix, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * passes * parts * kRadix, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * passes, st));
+  int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
+  k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, hist);
+  // Which digits actually vary? (a single populated bin = identity pass)
+  s.host_hist.resize((size_t)passes * kRadix);
+  DSG_CUDA_CHECK(cudaMemcpyAsync(s.host_hist.data(), hist, sizeof(uint32_t) * passes * kRadix,
+                                 cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::vector<bool> trivial(passes, false);
+  for (int p = 0; p < passes; ++p)
+    for (int d = 0; d < kRadix; ++d)
+      if (s.host_hist[(size_t)p * kRadix + d] == (uint32_t)n) trivial[p] = true;
+  k_hist_scan<<<passes, kRadix, 0, st>>>(hist);
+  const size_t smem = sizeof(OnesweepSmem<K>);
+  DSG_CUDA_CHECK(cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  bool in_alt = false;
+  for (int p = 0; p < passes; ++p) {
+    if (trivial[p]) continue;
+    const K* ki = in_alt ? keys_alt : keys;
+    const uint32_t* vi = in_alt ? vals_alt : vals;
+    K* ko = in_alt ? keys : keys_alt;
+    uint32_t* vo = in_alt ? vals : vals_alt;
+    k_onesweep<K><<<(unsigned)parts, kSortThreads, smem, st>>>(
+        ki, vi, ko, vo, n, begin_bit + kRadixBits * p, hist + (size_t)p * kRadix,
+        status + (size_t)p * parts * kRadix, counters + p);
+    in_alt = !in_alt;
+  }
+  DSG_CUDA_CHECK(cudaGetLastError());
+  return in_alt;
+}
+
+template bool radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t, int,
+                                         int, SortScratch&, cudaStream_t);
+template bool radix_sort_pairs<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, int64_t, int,
+                                         int, SortScratch&, cudaStream_t);
+
+}  // namespace dsg
