@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark: distributed 3DGS partition training on B200 (BASELINE.json metric).
+
+One "step" is one training iteration of one partition (trainer.hpp:173-207):
+render -> masked L1 + D-SSIM -> backward -> Adam, on one 1024^2 view.
+
+Workload (default ``kingsnake``, BASELINE configs[1] at N=1): a
+Kingsnake-shaped synthetic isosurface of 4M Gaussians per GPU, 448-view
+orbital rig (28 az x 16 el) at 1024^2, 10% test split, GT splats at the
+median NN spacing (opacity 0.97), kNN seeds, 2+2 px background masks
+(runtime.hpp:190-232). At N GPUs the cloud has N x 4M points and is cut
+into N slab partitions with 3 x NN ghost margins; rank k trains partition
+k with no communication (weak scaling).
+
+value  : whole-job training iterations/s, device-timed (CUDA events inside
+         dsg_train, max over ranks), inputs resident in HBM.
+e2e    : same through the public C ABI with host buffers: model uploaded
+         from host doubles, each step's view streamed from pinned host
+         memory, each step's loss read back, model downloaded at the end.
+--impl reference : the reference's own CPU implementation (oracle/_ref, the
+         unmodified headers compiled here) timed on the host cores, one
+         iteration per step on the same partition and views.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2509_12138_b200 import api, scenes  # noqa: E402
+from paper_2509_12138_b200.partition import partition_cloud  # noqa: E402
+from paper_2509_12138_b200.types import RenderConfig, SplatModel, TrainConfig, TrainView  # noqa: E402
+
+METRIC = "training iters/sec & Gaussians·views/sec at 1/2/4/8 B200; render Mpix/s"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+class Dist:
+    """Rank plumbing: torch.distributed (NCCL) only for barrier + max."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(self.local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            self.torch, self.dist = torch, dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self.torch.tensor([v], dtype=self.torch.float64, device=f"cuda:{self.local}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.out = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thr = threading.Thread(target=self._read, daemon=True)
+            self.thr.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.out.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thr.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.out:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        med = float(np.median(sm)) if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def build_partition_inputs(args, dist: Dist, ctx):
+    """Cloud -> auto values -> partition -> this rank's seeds + train views."""
+    n_total = args.n_per_gpu * dist.world
+    t0 = time.time()
+    if args.workload == "kingsnake":
+        pts, cols, _ = scenes.kingsnake(n_total, seed=1, turns=6.0 * dist.world,
+                                        length=1.0 * dist.world)
+    else:
+        pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
+    nn = api.median_nn_spacing(pts, ctx=ctx)          # resolve_auto_values (runtime.hpp:73-77)
+    margin = 3.0 * nn
+    parts = partition_cloud(pts, dist.world, margin)   # partition.hpp:42-104
+    part = parts[dist.rank]
+    idx = np.concatenate([part.owned_indices, part.ghost_indices]).astype(np.int64)
+    ppts, pcols = np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx])
+    rig = scenes.rig_for_cloud(pts, args.az, args.el, args.res)
+    n_rig = len(rig)
+    train_idx, test_idx = split_rig(n_rig, 0.1, 1)
+    cams = [rig[i] for i in train_idx]
+    rcfg = RenderConfig()
+    gt_model = api.ground_truth_model(ppts, pcols, nn, 0.97, ctx=ctx)
+    views = api.DeviceViews.synthesize(ctx, gt_model, rcfg, cams, ppts, True, 2.0, 2.0)
+    seeds = api.seed_gaussians(ppts, pcols, 3, ctx=ctx)
+    log(f"[rank {dist.rank}] inputs: cloud {n_total:,} pts, partition {len(ppts):,} "
+        f"({len(part.owned_indices):,} owned + {len(part.ghost_indices):,} ghosts), nn {nn:.6g}, "
+        f"{len(cams)} train views at {args.res}^2, setup {time.time() - t0:.1f}s")
+    return dict(points=ppts, colors=pcols, cams=cams, views=views, seeds=seeds, gt=gt_model,
+                rcfg=rcfg, nn=nn, n_part=len(ppts), rig=rig, test_idx=test_idx)
+
+
+def split_rig(n_views: int, test_fraction: float, seed: int):
+    """split_rig (camera.hpp:116-130): seeded Fisher-Yates, test = tail."""
+    M = (1 << 64) - 1
+
+    def mix(s):
+        s = (s + 0x9E3779B97F4A7C15) & M
+        z = s
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return s, z ^ (z >> 31)
+
+    s = (seed ^ 0x5E1170F5 ^ 0x853C49E6748FEA9B) & M
+    s, _ = mix(s)
+    s, _ = mix(s)
+    idx = list(range(n_views))
+    for i in range(n_views, 1, -1):
+        s, z = mix(s)
+        j = z % i
+        idx[i - 1], idx[j] = idx[j], idx[i - 1]
+    nt = 0
+    if test_fraction > 0 and n_views > 1:
+        nt = min(max(int(math.floor(test_fraction * n_views + 0.5)), 1), n_views - 1)
+    return idx[: n_views - nt], idx[n_views - nt:]
+
+
+def train_config(args, rank: int, iterations: int) -> TrainConfig:
+    # run_worker: cfg = spec.train, render = spec.render, seed = job seed + k (runtime.hpp:228-232)
+    return TrainConfig(iterations=iterations, seed=1 + rank)
+
+
+def roofline_for(stage: str, ms: float, n: int, npix: int, n_dup: int, peak: float):
+    """Algorithmic bytes per launch for the HBM-bound kernels."""
+    per = {
+        "adam": 412.0 * n,              # p,g,m,v read 224 B, p,m,v write 168 B, stats 20 B
+        "preprocess": 140.0 * n,        # params 56 B read, payload 84 B write
+        "chain": (56.0 + 56.0 + 12.0) * n + 40.0 * n_dup,
+        "loss": 37.0 * npix,
+    }
+    if stage not in per or ms <= 0:
+        return None
+    b = per[stage]
+    gbs = b / (ms * 1e-3) / 1e9
+    return {"bound": "hbm", "kernel": stage, "achieved": round(gbs, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(gbs / peak, 4), "bytes_per_launch": b, "traffic": None}
+
+
+def load_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM, "fallback"
+
+
+def run_ours(args, dist: Dist):
+    ctx = api.Context(dist.local)
+    inp = build_partition_inputs(args, dist, ctx)
+    seeds_host = inp["seeds"].download()           # the partition's seed model (host doubles)
+    n = len(seeds_host)
+    dm = api.DeviceModel(ctx, seeds_host)
+    views = inp["views"]
+    npix = args.res * args.res
+
+    # warm-up (untimed), then exactly K timed steps in one dsg_train call
+    if args.warmup > 0:
+        api.train_device(dm, views, train_config(args, dist.rank, args.warmup))
+        dm.upload(seeds_host)
+    ctx.synchronize()
+    clocks = ClockSampler(dist.local)
+    clocks.start()
+    dist.barrier()
+    ctx.synchronize()
+    w0 = time.perf_counter()
+    launches0 = api.launch_count()
+    fl, _ = api.train_device(dm, views, train_config(args, dist.rank, args.steps))
+    ctx.synchronize()
+    launches = api.launch_count() - launches0
+    dist.barrier()
+    wall = time.perf_counter() - w0
+    clk = clocks.stop()
+    dev_ms, _ = ctx.last_timing()
+    t_max = dist.max(dev_ms) / 1e3
+    wall_max = dist.max(wall)
+    total_iters = args.steps * dist.world
+    gv = dist.sum(float(n) * args.steps) / t_max
+
+    # per-stage profile (separate run; events + sync per step)
+    ctx.set_profiling(True)
+    dm.upload(seeds_host)
+    pk = max(3, min(args.steps, 8))
+    api.train_device(dm, views, train_config(args, dist.rank, pk))
+    prof_total, stages = ctx.last_timing()
+    ctx.set_profiling(False)
+    stage_ms = {s: float(v) / pk for s, v in zip(api.STAGES, stages)}
+    n_dup = api.frame_stats(ctx)["n_dup"]
+
+    # render Mpix/s on the test views (forward only, device-timed)
+    test_cams = [inp["rig"][i] for i in inp["test_idx"]]
+    r_ms = api.render_timed(dm, test_cams, inp["rcfg"], repeats=2)
+    mpix = len(test_cams) * 2 * npix / (r_ms * 1e-3) / 1e6
+    mpix = dist.sum(mpix)
+
+    # end-to-end through the C ABI with host buffers
+    order = api.view_order(train_config(args, dist.rank, 1).seed, len(views), args.steps)
+    gts, masks = [None] * len(views), [None] * len(views)
+    for vi in sorted(set(order.tolist())):
+        tv = views.download(int(vi))
+        gts[vi] = api.pinned(np.ascontiguousarray(tv.ground_truth.transpose(2, 0, 1), np.float32))
+        masks[vi] = api.pinned((tv.mask >= 0.5).astype(np.uint8))
+    hv = api.HostViews(ctx, views.cams, gts, masks)
+    host_params = np.ascontiguousarray(seeds_host.params)
+    dm_e = api.DeviceModel(ctx)
+    dist.barrier()
+    ctx.synchronize()
+    e0 = time.perf_counter()
+    dm_e.upload(SplatModel(host_params))
+    api.train_device(dm_e, hv, train_config(args, dist.rank, args.steps))
+    out = dm_e.download()
+    e_wall = time.perf_counter() - e0
+    e_max = dist.max(e_wall)
+    view_bytes = npix * (3 * 4 + 1)
+    h2d = view_bytes + n * 14 * 8 / args.steps
+    d2h = 8 + n * 14 * 8 / args.steps
+    del out
+
+    peak, peak_kind = load_peak()
+    dom = max(stage_ms, key=stage_ms.get)
+    hbm_stages = [s for s in ("adam", "preprocess", "chain", "loss") if stage_ms.get(s, 0) > 0]
+    dom_hbm = max(hbm_stages, key=lambda s: stage_ms[s]) if hbm_stages else None
+    roof = roofline_for(dom_hbm, stage_ms[dom_hbm], n, npix, n_dup, peak) if dom_hbm else None
+    if roof:
+        roof["peak_kind"] = peak_kind
+        roof["note"] = (f"dominant HBM-bound kernel; step-dominant stage is {dom} "
+                        f"({stage_ms[dom]:.3f} ms of {prof_total / pk:.3f} ms, FP32/issue-bound blend)")
+
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(inp, views, seeds_host, args)
+
+    line = {
+        "metric": METRIC,
+        "value": round(total_iters / t_max, 3),
+        "unit": "it/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t_max * 1e3 / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 (fp64 for ordering/cutoff decisions, SSIM statistics and the 3D chain)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}-shaped isosurface, {args.n_per_gpu:,} Gaussians/GPU "
+                               f"(+ghosts), {args.az}x{args.el} rig at {args.res}^2, one slab "
+                               f"partition per GPU", "gaussians_per_gpu": n,
+                   "views": len(views), "resolution": args.res, "partitions": dist.world,
+                   "l2": "working set > L2 (params+grads+moments 224 B/G)"},
+        "gaussian_views_per_sec": round(gv, 1),
+        "render_mpix_per_sec": round(mpix, 2),
+        "wall_s": round(wall_max, 4),
+        "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+        "n_dup": n_dup,
+        "e2e": {"value": round(total_iters / e_max, 3), "unit": "it/s",
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": int(dist.sum(float(launches))),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+        "final_loss": fl,
+    }
+    return line
+
+
+def cpu_baseline(inp, views, seeds_host, args):
+    """Reference CPU train iterations on a bounded sample: 1 iteration, 1 view."""
+    from oracle import Oracle, Reference, has_reference
+    impl = Reference() if has_reference() else Oracle()
+    kind = "reference" if has_reference() else "port"
+    cores = os.cpu_count() or 1
+    order = api.view_order(1, len(views), 1)
+    tv = views.download(int(order[0]))
+    cfg = TrainConfig(iterations=1, seed=1)
+    t0 = time.perf_counter()
+    impl.train_partition_full(seeds_host, [tv], cfg, shards=cores)
+    dt = time.perf_counter() - t0
+    return {"value": round(1.0 / dt, 5), "unit": "it/s", "cores": cores, "kind": kind,
+            "sample": f"1 training iteration of the same partition ({len(seeds_host):,} Gaussians) "
+                      f"on 1 {args.res}^2 view, shards={cores} (row-band threads), {dt:.1f} s",
+            "gaussian_views_per_sec": round(len(seeds_host) / dt, 1)}
+
+
+def run_reference(args, dist: Dist):
+    if dist.rank != 0:
+        return None
+    from oracle import Oracle, Reference, has_reference
+    impl = Reference() if has_reference() else Oracle()
+    kind = "reference" if has_reference() else "port"
+    ctx = api.Context(dist.local)
+    inp = build_partition_inputs(args, _single(), ctx)
+    seeds_host = inp["seeds"].download()
+    views = inp["views"]
+    cores = os.cpu_count() or 1
+    order = api.view_order(1, len(views), args.warmup + args.steps)
+    for it in range(args.warmup):
+        tv = views.download(int(order[it]))
+        impl.train_partition_full(seeds_host, [tv], TrainConfig(iterations=1, seed=1), shards=cores)
+    dts = []
+    for it in range(args.steps):
+        tv = views.download(int(order[args.warmup + it]))
+        t0 = time.perf_counter()
+        impl.train_partition_full(seeds_host, [tv], TrainConfig(iterations=1, seed=1), shards=cores)
+        dts.append(time.perf_counter() - t0)
+    T = float(sum(dts))
+    v = args.steps / T
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "it/s",
+        "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(T * 1e3 / args.steps, 2), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload}-shaped isosurface, {args.n_per_gpu:,} Gaussians "
+                               f"(partition 0), {args.res}^2 views", "gaussians": len(seeds_host)},
+        "gaussian_views_per_sec": round(len(seeds_host) * v, 1),
+        "cpu_baseline": {"value": round(v, 5), "unit": "it/s", "cores": cores, "kind": kind,
+                         "sample": f"each step = 1 reference training iteration (render, loss, "
+                                   f"backward, Adam) of the full partition on one view, shards={cores}"},
+        "e2e": {"value": round(v, 5), "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def _single():
+    d = Dist.__new__(Dist)
+    d.world, d.rank, d.local, d.pg = 1, 0, int(os.environ.get("LOCAL_RANK", "0")), None
+    return d
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=list(scenes.SIZES), default="kingsnake")
+    ap.add_argument("--n-per-gpu", type=int, default=None)
+    ap.add_argument("--res", type=int, default=1024)
+    ap.add_argument("--az", type=int, default=28)
+    ap.add_argument("--el", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.n_per_gpu is None:
+        args.n_per_gpu = scenes.SIZES[args.workload]
+    dist = Dist()
+    if args.gpus != dist.world:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {dist.world}; using WORLD_SIZE")
+    if args.impl == "reference":
+        line = run_reference(args, dist)
+    else:
+        line = run_ours(args, dist)
+    if dist.rank == 0 and line is not None:
+        print(json.dumps(line), flush=True)
+    dist.close()
+
+
+if __name__ == "__main__":
+    main()

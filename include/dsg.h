@@ -138,6 +138,19 @@ int dsg_backward(dsg_ctx ctx, dsg_model model, const dsg_camera* cam,
 int dsg_adam_step(dsg_ctx ctx, dsg_model model, const double* grads,
                   const dsg_group_rates* rates, const dsg_adam_config* adam);
 
+/* ---- seeding (seed.hpp) ---------------------------------------------------- */
+/* knn_mean_distances (seed.hpp:16-35): exact grid k-NN, fp64 distances. */
+int dsg_knn_mean(dsg_ctx ctx, const double* points, int64_t n, int32_t k, double* out);
+/* median_nn_spacing (seed.hpp:39-45). */
+int dsg_median_nn_spacing(dsg_ctx ctx, const double* points, int64_t n, double* out);
+/* seed_gaussians (seed.hpp:49-74) straight into a device model.
+ * rule: 0 = ScaleRule::Knn (k neighbours), 1 = ScaleRule::Fixed. */
+int dsg_seed_gaussians(dsg_ctx ctx, const double* points, const double* colors, int64_t n,
+                       int32_t rule, int32_t k, double fixed_scale, dsg_model model);
+/* ground_truth_model (seed.hpp:78-94) straight into a device model. */
+int dsg_ground_truth_model(dsg_ctx ctx, const double* points, const double* colors, int64_t n,
+                           double scale, double opacity, dsg_model model);
+
 /* ---- training -------------------------------------------------------------- */
 /* Train views (TrainView, loss.hpp:14-26) resident on the device: ground
  * truth [v][h][w][3] and masks [v][h][w] doubles; all views share (w, h). */
@@ -149,7 +162,16 @@ int dsg_views_synthesize(dsg_ctx ctx, dsg_model gt_model, const dsg_render_confi
                          const dsg_camera* cams, int32_t n_views, const double* points,
                          int64_t n_points, int32_t use_masks, double footprint_px,
                          double dilation_px, dsg_views* out);
+/* Views left in caller-owned (pinned) host memory, streamed to the device
+ * one step at a time by dsg_train (the end-to-end path): gt_planar[v] is
+ * [3][h*w] float, masks[v] is [h*w] bytes; entries the schedule never uses
+ * may be NULL. The caller keeps the memory alive until dsg_views_destroy. */
+int dsg_views_create_host(dsg_ctx ctx, const dsg_camera* cams, const float* const* gt_planar,
+                          const uint8_t* const* masks, int32_t n_views, dsg_views* out);
 int dsg_views_destroy(dsg_views views);
+/* The view index used at each of `iterations` steps for a seed
+ * (trainer.hpp:157-163, 174). */
+int dsg_view_order(uint64_t seed, int32_t n_views, int64_t iterations, int32_t* out);
 /* Copy view v back (gt [h][w][3], mask [h][w]; either may be NULL). */
 int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t v, double* ground_truth,
                        double* mask);
@@ -163,11 +185,25 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
               int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
               double* loss_trace);
 
+/* Number of this library's kernel launches so far (process-wide). */
+int64_t dsg_launch_count(void);
+/* Visible splats and tile duplicates of the last view binned on ctx. */
+int dsg_frame_stats(dsg_ctx ctx, int64_t* n_visible, int64_t* n_dup);
+/* Forward-render n cameras `repeats` times back to back on the device;
+ * *ms = CUDA-event time (render Mpix/s measurement). */
+int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32_t n,
+                     const dsg_render_config* cfg, int32_t repeats, double* ms);
+/* Page-lock caller memory for the end-to-end path (cudaHostRegister). */
+int dsg_host_register(void* ptr, int64_t bytes);
+int dsg_host_unregister(void* ptr);
+
 /* Record per-stage CUDA events inside dsg_train (adds one sync per step). */
 int dsg_set_profiling(dsg_ctx ctx, int32_t enable);
 
-/* CUDA-event device time (ms) of the last dsg_train call and the per-stage
- * totals {preprocess+sort, blend fwd, loss, blend bwd, chain, adam}. */
+/* CUDA-event device time (ms) of the last dsg_train call and, when
+ * profiling was on, the per-stage totals (9 entries): preprocess, depth
+ * sort, scan+duplicate, tile sort+ranges, blend fwd, loss, blend bwd,
+ * 3D chain, Adam. */
 int dsg_last_timing(dsg_ctx ctx, double* total_ms, double* stage_ms);
 
 #ifdef __cplusplus

@@ -147,9 +147,13 @@ class Context:
 
     def last_timing(self):
         tot = C.c_double()
-        st = np.zeros(6)
+        st = np.zeros(len(STAGES))
         _check(lib().dsg_last_timing(self.h, C.byref(tot), _p(st)))
         return tot.value, st
+
+
+STAGES = ("preprocess", "depth_sort", "scan_duplicate", "tile_sort_ranges", "blend_fwd", "loss",
+          "blend_bwd", "chain", "adam")
 
 
 class DeviceModel:
@@ -402,3 +406,103 @@ def train_partition(model: SplatModel, views, cfg: TrainConfig, shards: int = 1,
                     ctx: Context = None) -> SplatModel:
     """train_partition (trainer.hpp:214-217)."""
     return train_partition_full(model, views, cfg, shards, ctx=ctx).model
+
+
+# ---- seeding (seed.hpp) ---------------------------------------------------------
+def knn_mean_distances(points, k: int, ctx: Context = None):
+    """knn_mean_distances (seed.hpp:16-35): exact grid k-NN on the device."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    out = np.zeros(max(pts.shape[0], 1))
+    _check(lib().dsg_knn_mean(ctx.h, _p(pts), C.c_int64(pts.shape[0]), C.c_int32(k), _p(out)))
+    return out[: pts.shape[0]]
+
+
+def median_nn_spacing(points, ctx: Context = None) -> float:
+    """median_nn_spacing (seed.hpp:39-45)."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    out = C.c_double()
+    _check(lib().dsg_median_nn_spacing(ctx.h, _p(pts), C.c_int64(pts.shape[0]), C.byref(out)))
+    return out.value
+
+
+def seed_gaussians(points, colors, k: int = 3, ctx: Context = None, fixed_scale=None) -> DeviceModel:
+    """seed_gaussians(pc, Knn, k) / (Fixed, fixed_scale) into a device model (seed.hpp:49-74)."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    col = np.ascontiguousarray(colors, dtype=np.float64).reshape(-1, 3)
+    dm = DeviceModel(ctx)
+    rule = 1 if fixed_scale is not None else 0
+    _check(lib().dsg_seed_gaussians(ctx.h, _p(pts), _p(col), C.c_int64(pts.shape[0]),
+                                    C.c_int32(rule), C.c_int32(k),
+                                    C.c_double(fixed_scale or 0.01), dm.h))
+    return dm
+
+
+def ground_truth_model(points, colors, scale: float, opacity: float = 0.97,
+                       ctx: Context = None) -> DeviceModel:
+    """ground_truth_model (seed.hpp:78-94) into a device model."""
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    col = np.ascontiguousarray(colors, dtype=np.float64).reshape(-1, 3)
+    dm = DeviceModel(ctx)
+    _check(lib().dsg_ground_truth_model(ctx.h, _p(pts), _p(col), C.c_int64(pts.shape[0]),
+                                        C.c_double(scale), C.c_double(opacity), dm.h))
+    return dm
+
+
+def view_order(seed: int, n_views: int, iterations: int):
+    """View index per step (trainer.hpp:157-163, 174)."""
+    out = np.zeros(max(iterations, 1), np.int32)
+    _check(lib().dsg_view_order(C.c_uint64(seed), C.c_int32(n_views), C.c_int64(iterations),
+                                _p(out, C.c_int32)))
+    return out[:iterations]
+
+
+class HostViews(DeviceViews):
+    """Views kept in pinned host memory and streamed per step (end-to-end path).
+
+    ``gts[v]`` is a (3, h, w) float32 planar array and ``masks[v]`` an (h, w)
+    uint8 array (either may be None for views the schedule never touches);
+    both must stay alive (and ideally be pinned) while the object lives.
+    """
+
+    def __init__(self, ctx: Context, cams, gts, masks):
+        n = len(cams)
+        carr = (dsg_camera * n)(*[cam_struct(c) for c in cams])
+        gp = (C.c_void_p * n)(*[None if g is None else g.ctypes.data for g in gts])
+        mp = (C.c_void_p * n)(*[None if m is None else m.ctypes.data for m in masks])
+        h = C.c_void_p()
+        _check(lib().dsg_views_create_host(ctx.h, carr, gp, mp, C.c_int32(n), C.byref(h)))
+        self._keep = (gts, masks)
+        super().__init__(ctx, h, list(cams), cams[0].width, cams[0].height)
+
+
+def launch_count() -> int:
+    L = lib()
+    L.dsg_launch_count.restype = C.c_int64
+    return int(L.dsg_launch_count())
+
+
+def frame_stats(ctx: Context):
+    nv, nd = C.c_int64(), C.c_int64()
+    _check(lib().dsg_frame_stats(ctx.h, C.byref(nv), C.byref(nd)))
+    return {"n_visible": nv.value, "n_dup": nd.value}
+
+
+def render_timed(dmodel: DeviceModel, cams, cfg: RenderConfig, repeats: int = 1) -> float:
+    """Device ms to forward-render `cams` `repeats` times (render Mpix/s)."""
+    n = len(cams)
+    carr = (dsg_camera * n)(*[cam_struct(c) for c in cams])
+    ms = C.c_double()
+    _check(lib().dsg_render_timed(dmodel.ctx.h, dmodel.h, carr, C.c_int32(n),
+                                  C.byref(cfg_struct(cfg)), C.c_int32(repeats), C.byref(ms)))
+    return ms.value
+
+
+def pinned(a: np.ndarray) -> np.ndarray:
+    """Page-lock a numpy array in place (kept registered for its lifetime)."""
+    a = np.ascontiguousarray(a)
+    _check(lib().dsg_host_register(C.c_void_p(a.ctypes.data), C.c_int64(a.nbytes)))
+    return a

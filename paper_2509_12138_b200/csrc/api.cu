@@ -5,6 +5,8 @@
 // (adam.hpp:55) and train_partition_full (trainer.hpp:140) over device-
 // resident models and views. Validation order and messages follow the
 // reference so the C++ wrappers can rethrow identical dsplat::Error texts.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -25,6 +27,9 @@ static const char* kCodeNames[] = {
     "MissingBaseline", "InvalidArgument"};
 
 void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+static std::atomic<int64_t> g_launches{0};
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void throw_cuda(cudaError_t e, const char* expr, const char* file, int line) {
   char buf[512];
@@ -62,9 +67,13 @@ struct dsg_ctx_s {
   DevBuf<float> stage_f;
   DevBuf<uint8_t> stage_u8;
   DevBuf<double> loss_trace;
-  std::vector<cudaEvent_t> events;
+  StageTimer timer;
+  bool timer_init = false;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  double* host_loss = nullptr;  // pinned, end-to-end mode
   double last_total_ms = 0.0;
-  double last_stage_ms[6] = {0, 0, 0, 0, 0, 0};
+  int64_t last_iters = 0;
+  double last_stage_ms[StageTimer::kStages] = {};
   bool profile = false;
 };
 
@@ -76,8 +85,11 @@ struct dsg_views_s {
   int32_t n = 0;
   int width = 0, height = 0;
   std::vector<dsg_camera> cams;
-  DevBuf<float> gt;       // [v][3][npix]
+  DevBuf<float> gt;       // [v][3][npix] (host mode: one staging slot)
   DevBuf<uint8_t> mask;   // [v][npix]
+  bool host = false;      // views live in caller-owned pinned host memory
+  std::vector<const float*> host_gt;
+  std::vector<const uint8_t*> host_mask;
 };
 
 namespace {
@@ -233,6 +245,7 @@ void forward(dsg_ctx ctx, ModelDev& m, const CamDev& cam, const RenderDev& rd) {
     k_fill_bg<<<nblk(npix), 256, 0, ctx->stream>>>(f.rgb.get(), f.T.get(), f.last.get(),
                                                    f.ncontrib.get(), npix, rd.bg[0], rd.bg[1],
                                                    rd.bg[2]);
+                                                   count_launch();
     return;
   }
   blend_forward(f, m.params.get(), m.cap, cam, rd, ctx->stream);
@@ -355,7 +368,12 @@ int dsg_ctx_destroy(dsg_ctx ctx) {
     if (!ctx) return;
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    for (auto e : ctx->events) cudaEventDestroy(e);
+    if (ctx->timer_init) {
+      for (int k = 0; k <= StageTimer::kStages; ++k) cudaEventDestroy(ctx->timer.ev[k]);
+      cudaEventDestroy(ctx->ev_begin);
+      cudaEventDestroy(ctx->ev_end);
+    }
+    if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -394,6 +412,7 @@ int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t
       DSG_CUDA_CHECK(cudaMemcpyAsync(st, params, sizeof(double) * kParams * n, cudaMemcpyHostToDevice,
                                      ctx->stream));
       k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
+      count_launch();
     }
     reset_optimizer(ctx, m);
     DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -412,6 +431,7 @@ int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t cap
     if (capacity < m.n) fail(kInvalidArgument, "output capacity too small");
     double* st = ctx->stage_d.ensure(kParams * m.n);
     k_planar_to_aos<<<nblk(m.n), 256, 0, ctx->stream>>>(m.params.get(), m.cap, m.n, kParams, st);
+    count_launch();
     DSG_CUDA_CHECK(cudaMemcpyAsync(params, st, sizeof(double) * kParams * m.n, cudaMemcpyDeviceToHost,
                                    ctx->stream));
     DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -438,6 +458,7 @@ int dsg_model_adam_state(dsg_ctx ctx, dsg_model model, double* mo, double* vo, i
       if (!out) continue;
       k_planar_to_aos<<<nblk(m.n), 256, 0, ctx->stream>>>(w == 0 ? m.m.get() : m.v.get(), m.cap,
                                                           m.n, kParams, st);
+                                                          count_launch();
       DSG_CUDA_CHECK(cudaMemcpyAsync(out, st, sizeof(double) * kParams * m.n,
                                      cudaMemcpyDeviceToHost, ctx->stream));
       DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -460,6 +481,7 @@ int dsg_render(dsg_ctx ctx, dsg_model model, const dsg_camera* cam_in,
     if (rgb || alpha) {
       double* d = ctx->stage_d.ensure(4 * npix);
       k_render_out<<<nblk(npix), 256, 0, st>>>(f.rgb.get(), f.T.get(), npix, d, d + 3 * npix);
+      count_launch();
       if (rgb)
         DSG_CUDA_CHECK(cudaMemcpyAsync(rgb, d, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, st));
       if (alpha)
@@ -517,10 +539,14 @@ int dsg_masked_loss(dsg_ctx ctx, const double* rendered, const double* ground_tr
     float* gt = ctx->stage_f.ensure(3 * npix);
     uint8_t* m8 = ctx->stage_u8.ensure(npix);
     k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d, npix, 3, f.rgb.get(), npix);
+    count_launch();
     k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d + 3 * npix, npix, 3, gt, npix);
+    count_launch();
     k_mask_u8<<<nblk(npix), 256, 0, st>>>(d + 6 * npix, npix, m8);
+    count_launch();
     masked_loss_dev(f, gt, m8, width, height, loss_lambda, st);
     k_planar_to_aos<<<nblk(npix), 256, 0, st>>>(f.dL.get(), npix, npix, 3, d);
+    count_launch();
     DSG_CUDA_CHECK(cudaMemcpyAsync(dL_dpixels, d, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, st));
     DSG_CUDA_CHECK(cudaMemcpyAsync(loss, f.loss_out.get(), sizeof(double), cudaMemcpyDeviceToHost, st));
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -549,15 +575,18 @@ int dsg_backward(dsg_ctx ctx, dsg_model model, const dsg_camera* cam_in,
     DSG_CUDA_CHECK(cudaMemcpyAsync(d, dL_dpixels, sizeof(double) * 3 * npix, cudaMemcpyHostToDevice, st));
     f.dL.ensure(3 * npix);
     k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d, npix, 3, f.dL.get(), npix);
+    count_launch();
     backward_dev(ctx, m, cam, rd);
     if (m.n > 0) {
       if (grads) {
         k_planar_to_aos<<<nblk(m.n), 256, 0, st>>>(m.grads.get(), m.cap, m.n, kParams, d);
+        count_launch();
         DSG_CUDA_CHECK(cudaMemcpyAsync(grads, d, sizeof(double) * kParams * m.n, cudaMemcpyDeviceToHost, st));
         DSG_CUDA_CHECK(cudaStreamSynchronize(st));
       }
       if (d_mean2d) {
         k_planar_to_aos<<<nblk(m.n), 256, 0, st>>>(m.dmean.get(), m.cap, m.n, 2, d);
+        count_launch();
         DSG_CUDA_CHECK(cudaMemcpyAsync(d_mean2d, d, sizeof(double) * 2 * m.n, cudaMemcpyDeviceToHost, st));
         DSG_CUDA_CHECK(cudaStreamSynchronize(st));
       }
@@ -580,6 +609,7 @@ int dsg_adam_step(dsg_ctx ctx, dsg_model model, const double* grads, const dsg_g
     double* d = ctx->stage_d.ensure(kParams * m.n);
     DSG_CUDA_CHECK(cudaMemcpyAsync(d, grads, sizeof(double) * kParams * m.n, cudaMemcpyHostToDevice, st));
     k_aos_to_planar<<<nblk(m.n), 256, 0, st>>>(d, m.n, kParams, m.grads.get(), m.cap);
+    count_launch();
     double r[5] = {rates->mu, rates->log_scale, rates->rot, rates->opacity, rates->color};
     adam_update(make_adam(m, r, *adam, m.adam_step, false), st);
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -612,7 +642,9 @@ int dsg_views_create(dsg_ctx ctx, const dsg_camera* cams, const double* ground_t
           DSG_CUDA_CHECK(cudaMemcpyAsync(d + 3 * npix, masks + npix * i, sizeof(double) * npix,
                                          cudaMemcpyHostToDevice, ctx->stream));
           k_aos_to_planar<<<nblk(npix), 256, 0, ctx->stream>>>(d, npix, 3, v->gt.get() + 3 * npix * i, npix);
+          count_launch();
           k_mask_u8<<<nblk(npix), 256, 0, ctx->stream>>>(d + 3 * npix, npix, v->mask.get() + npix * i);
+          count_launch();
         }
         DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       }
@@ -638,6 +670,7 @@ int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t i, double* ground_t
     if (ground_truth) {
       k_planar_to_aos<<<nblk(npix), 256, 0, ctx->stream>>>(views->gt.get() + 3 * npix * i, npix,
                                                            npix, 3, d);
+                                                           count_launch();
       DSG_CUDA_CHECK(cudaMemcpyAsync(ground_truth, d, sizeof(double) * 3 * npix,
                                      cudaMemcpyDeviceToHost, ctx->stream));
       DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
@@ -649,6 +682,48 @@ int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t i, double* ground_t
       DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       for (int64_t k = 0; k < npix; ++k) mask[k] = m8[k] ? 1.0 : 0.0;
     }
+  });
+}
+
+int dsg_view_order(uint64_t seed, int32_t n_views, int64_t iterations, int32_t* out) {
+  return guarded([&] {  // trainer.hpp:157-163, 174
+    if (n_views <= 0) fail(kNoViews, "training requires at least one view");
+    std::vector<int32_t> order(n_views);
+    std::iota(order.begin(), order.end(), 0);
+    Rng vr(seed ^ 0x87aa11d3ULL);
+    for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[(size_t)vr.below(i)]);
+    for (int64_t it = 0; it < iterations; ++it) out[it] = order[(size_t)(it % n_views)];
+  });
+}
+
+int dsg_views_create_host(dsg_ctx ctx, const dsg_camera* cams, const float* const* gt_planar,
+                          const uint8_t* const* masks, int32_t n_views, dsg_views* out) {
+  return guarded([&] {
+    auto* v = new dsg_views_s();
+    try {
+      v->n = n_views;
+      v->host = true;
+      for (int32_t i = 0; i < n_views; ++i) {
+        make_cam(&cams[i]);
+        if (i == 0) {
+          v->width = cams[0].width;
+          v->height = cams[0].height;
+        } else if (cams[i].width != v->width || cams[i].height != v->height) {
+          fail(kDimensionMismatch, "all views must share one resolution");
+        }
+        v->cams.push_back(cams[i]);
+        v->host_gt.push_back(gt_planar ? gt_planar[i] : nullptr);
+        v->host_mask.push_back(masks ? masks[i] : nullptr);
+      }
+      DeviceGuard g(ctx->device);
+      const int64_t npix = (int64_t)v->width * v->height;
+      v->gt.ensure(std::max<int64_t>(1, 3 * npix));
+      v->mask.ensure(std::max<int64_t>(1, npix));
+    } catch (...) {
+      delete v;
+      throw;
+    }
+    *out = v;
   });
 }
 
@@ -676,75 +751,92 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     std::iota(order.begin(), order.end(), size_t{0});
     Rng vr(cfg->seed ^ 0x87aa11d3ULL);
     for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[(size_t)vr.below(i)]);
+    if (views->host)
+      for (int64_t it = 0; it < std::min<int64_t>(iters, views->n); ++it) {
+        size_t vi = order[(size_t)it];
+        if (!views->host_gt[vi] || !views->host_mask[vi])
+          fail(kInvalidArgument, "host view used by the schedule has no data");
+      }
 
     DeviceGuard g(ctx->device);
     cudaStream_t st = ctx->stream;
     reset_optimizer(ctx, m);   // fresh AdamState and stats (trainer.hpp:167-168)
     const int64_t npix = (int64_t)views->width * views->height;
     double* trace = ctx->loss_trace.ensure(iters);
-    const bool prof = ctx->profile;
-    if (ctx->events.size() < 8) {
-      for (size_t k = ctx->events.size(); k < 8; ++k) {
-        cudaEvent_t e;
-        DSG_CUDA_CHECK(cudaEventCreate(&e));
-        ctx->events.push_back(e);
-      }
+    StageTimer& tm = ctx->timer;
+    tm.on = ctx->profile;
+    if (!ctx->timer_init) {
+      for (int k = 0; k <= StageTimer::kStages; ++k) DSG_CUDA_CHECK(cudaEventCreate(&tm.ev[k]));
+      DSG_CUDA_CHECK(cudaEventCreate(&ctx->ev_begin));
+      DSG_CUDA_CHECK(cudaEventCreate(&ctx->ev_end));
+      ctx->timer_init = true;
     }
-    double stage[6] = {0, 0, 0, 0, 0, 0};
-    DSG_CUDA_CHECK(cudaEventRecord(ctx->events[7], st));
+    double stage[StageTimer::kStages] = {};
+    if (views->host && !ctx->host_loss) {
+      DSG_CUDA_CHECK(cudaMallocHost(&ctx->host_loss, sizeof(double)));
+    }
+    DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_begin, st));
     for (int64_t it = 0; it < iters; ++it) {
       const size_t vi = order[(size_t)it % order.size()];
       const CamDev& cam = cams[vi];
-      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[0], st));
-      bin_frame(ctx->frame, m.params.get(), m.cap, m.n, cam, rd, st);
+      const float* gt = views->gt.get() + (views->host ? 0 : 3 * npix * vi);
+      const uint8_t* mk = views->mask.get() + (views->host ? 0 : npix * vi);
+      if (views->host) {  // end-to-end mode: this step's view comes from pinned host memory
+        DSG_CUDA_CHECK(cudaMemcpyAsync(views->gt.get(), views->host_gt[vi], sizeof(float) * 3 * npix,
+                                       cudaMemcpyHostToDevice, st));
+        DSG_CUDA_CHECK(cudaMemcpyAsync(views->mask.get(), views->host_mask[vi], npix,
+                                       cudaMemcpyHostToDevice, st));
+      }
+      bin_frame(ctx->frame, m.params.get(), m.cap, m.n, cam, rd, st, &tm);
       Frame& f = ctx->frame;
-      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[1], st));
-      if (f.n_visible == 0 || f.n_dup == 0) {
+      const bool empty = f.n_visible == 0 || f.n_dup == 0;
+      if (empty) {
+        for (int k = 1; k <= 4; ++k) tm.mark(k, st);
         forward(ctx, m, cam, rd);
       } else {
         blend_forward(f, m.params.get(), m.cap, cam, rd, st);
       }
-      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[2], st));
-      masked_loss_dev(f, views->gt.get() + 3 * npix * vi, views->mask.get() + npix * vi,
-                      views->width, views->height, cfg->loss_lambda, st);
+      tm.mark(5, st);
+      masked_loss_dev(f, gt, mk, views->width, views->height, cfg->loss_lambda, st);
       DSG_CUDA_CHECK(cudaMemcpyAsync(trace + it, f.loss_out.get(), sizeof(double),
                                      cudaMemcpyDeviceToDevice, st));
-      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[3], st));
-      if (f.n_visible > 0 && f.n_dup > 0) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
-      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[4], st));
-      {
-        if (f.n_visible == 0 || f.n_dup == 0) {
-          DSG_CUDA_CHECK(cudaMemsetAsync(m.grads.get(), 0, sizeof(float) * kParams * m.cap, st));
-          DSG_CUDA_CHECK(cudaMemsetAsync(m.touch.get(), 0, sizeof(int32_t) * m.cap, st));
-          DSG_CUDA_CHECK(cudaMemsetAsync(m.dmean.get(), 0, sizeof(float) * 2 * m.cap, st));
-        } else {
-          ChainArgs a;
-          a.params = m.params.get();
-          a.pitch = m.cap;
-          a.n = m.n;
-          a.cam = cam;
-          a.tcount = f.tcount.get();
-          a.dup_base = f.dup_base.get();
-          a.partials = f.partials.get();
-          a.grads = m.grads.get();
-          a.dmean = m.dmean.get();
-          a.touch = m.touch.get();
-          chain_3d(a, st);
-        }
+      if (views->host)  // the step's result read back to the host
+        DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->host_loss, f.loss_out.get(), sizeof(double),
+                                       cudaMemcpyDeviceToHost, st));
+      tm.mark(6, st);
+      if (!empty) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
+      tm.mark(7, st);
+      if (empty) {
+        DSG_CUDA_CHECK(cudaMemsetAsync(m.grads.get(), 0, sizeof(float) * kParams * m.cap, st));
+        DSG_CUDA_CHECK(cudaMemsetAsync(m.touch.get(), 0, sizeof(int32_t) * m.cap, st));
+        DSG_CUDA_CHECK(cudaMemsetAsync(m.dmean.get(), 0, sizeof(float) * 2 * m.cap, st));
+      } else {
+        ChainArgs a;
+        a.params = m.params.get();
+        a.pitch = m.cap;
+        a.n = m.n;
+        a.cam = cam;
+        a.tcount = f.tcount.get();
+        a.dup_base = f.dup_base.get();
+        a.partials = f.partials.get();
+        a.grads = m.grads.get();
+        a.dmean = m.dmean.get();
+        a.touch = m.touch.get();
+        chain_3d(a, st);
       }
-      if (prof) DSG_CUDA_CHECK(cudaEventRecord(ctx->events[5], st));
+      tm.mark(8, st);
       const double decay = std::pow(cfg->lr_mu_decay, (double)it / (double)iters);
       const double rates[5] = {cfg->lr_mu * decay, cfg->lr_scale, cfg->lr_rot, cfg->lr_opacity,
                                cfg->lr_color};
       m.adam_step += 1;
       adam_update(make_adam(m, rates, cfg->adam, m.adam_step, true), st);
       m.iteration += 1;
-      if (prof) {
-        DSG_CUDA_CHECK(cudaEventRecord(ctx->events[6], st));
-        DSG_CUDA_CHECK(cudaEventSynchronize(ctx->events[6]));
+      tm.mark(9, st);
+      if (tm.on) {
+        DSG_CUDA_CHECK(cudaEventSynchronize(tm.ev[9]));
         float ms;
-        for (int s = 0; s < 6; ++s) {
-          DSG_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->events[s], ctx->events[s + 1]));
+        for (int s = 0; s < StageTimer::kStages; ++s) {
+          DSG_CUDA_CHECK(cudaEventElapsedTime(&ms, tm.ev[s], tm.ev[s + 1]));
           stage[s] += ms;
         }
       }
@@ -755,12 +847,13 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
         progress(it + 1, l, user);
       }
     }
-    DSG_CUDA_CHECK(cudaEventRecord(ctx->events[6], st));
-    DSG_CUDA_CHECK(cudaEventSynchronize(ctx->events[6]));
+    DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_end, st));
+    DSG_CUDA_CHECK(cudaEventSynchronize(ctx->ev_end));
     float total;
-    DSG_CUDA_CHECK(cudaEventElapsedTime(&total, ctx->events[7], ctx->events[6]));
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&total, ctx->ev_begin, ctx->ev_end));
     ctx->last_total_ms = total;
-    for (int s = 0; s < 6; ++s) ctx->last_stage_ms[s] = stage[s];
+    ctx->last_iters = iters;
+    for (int s = 0; s < StageTimer::kStages; ++s) ctx->last_stage_ms[s] = stage[s];
     std::vector<double> tr(iters);
     DSG_CUDA_CHECK(cudaMemcpy(tr.data(), trace, sizeof(double) * iters, cudaMemcpyDeviceToHost));
     if (final_loss) *final_loss = tr.back();
@@ -845,11 +938,129 @@ int dsg_views_synthesize(dsg_ctx ctx, dsg_model gt_model, const dsg_render_confi
   });
 }
 
+int dsg_knn_mean(dsg_ctx ctx, const double* points, int64_t n, int32_t k, double* out) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    if (n <= 0) return;
+    double* d = ctx->stage_d2.ensure(4 * n);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+    knn_mean_dev(points, d, n, k, d + 3 * n, ctx->frame.sort, ctx->stream);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(out, d + 3 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dsg_median_nn_spacing(dsg_ctx ctx, const double* points, int64_t n, double* out) {
+  return guarded([&] {  // seed.hpp:39-45
+    if (n <= 0) fail(kEmptyCloud, "empty point cloud");
+    if (n == 1) {
+      *out = 1.0;
+      return;
+    }
+    std::vector<double> nn(n);
+    DeviceGuard g(ctx->device);
+    double* d = ctx->stage_d2.ensure(4 * n);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, ctx->stream));
+    knn_mean_dev(points, d, n, 1, d + 3 * n, ctx->frame.sort, ctx->stream);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(nn.data(), d + 3 * n, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    std::nth_element(nn.begin(), nn.begin() + n / 2, nn.end());
+    *out = nn[(size_t)(n / 2)];
+  });
+}
+
+int dsg_seed_gaussians(dsg_ctx ctx, const double* points, const double* colors, int64_t n,
+                       int32_t rule, int32_t k, double fixed_scale, dsg_model model) {
+  return guarded([&] {  // seed.hpp:49-74
+    if (n <= 0) fail(kEmptyCloud, "cannot seed from an empty cloud");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    ModelDev& m = model->m;
+    m.reserve(n);
+    m.n = n;
+    m.iteration = 0;
+    m.origin_partition = -1;
+    double* d = ctx->stage_d2.ensure(7 * n);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d + 3 * n, colors, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    const double* scale = nullptr;
+    if (rule == 0 && n > 1) {
+      knn_mean_dev(points, d, n, k, d + 6 * n, ctx->frame.sort, st);
+      scale = d + 6 * n;
+    }
+    const double op = std::log(0.1 / (1.0 - 0.1));
+    seed_params_dev(d, d + 3 * n, scale, n, std::log(fixed_scale), op, m.params.get(), m.cap, st);
+    reset_optimizer(ctx, m);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int dsg_ground_truth_model(dsg_ctx ctx, const double* points, const double* colors, int64_t n,
+                           double scale, double opacity, dsg_model model) {
+  return guarded([&] {  // seed.hpp:78-94
+    if (n <= 0) fail(kEmptyCloud, "cannot build ground truth from nothing");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    ModelDev& m = model->m;
+    m.reserve(n);
+    m.n = n;
+    m.iteration = 0;
+    m.origin_partition = -1;
+    double* d = ctx->stage_d2.ensure(6 * n);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, points, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d + 3 * n, colors, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st));
+    seed_params_dev(d, d + 3 * n, nullptr, n, std::log(std::max(scale, 1e-7)),
+                    std::log(opacity / (1.0 - opacity)), m.params.get(), m.cap, st);
+    reset_optimizer(ctx, m);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int64_t dsg_launch_count(void) { return g_launches.load(); }
+
+int dsg_frame_stats(dsg_ctx ctx, int64_t* n_visible, int64_t* n_dup) {
+  return guarded([&] {
+    if (n_visible) *n_visible = ctx->frame.n_visible;
+    if (n_dup) *n_dup = ctx->frame.n_dup;
+  });
+}
+
+int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32_t n,
+                     const dsg_render_config* cfg, int32_t repeats, double* ms) {
+  return guarded([&] {
+    RenderDev rd = make_rd(cfg);
+    std::vector<CamDev> cv;
+    for (int32_t i = 0; i < n; ++i) cv.push_back(make_cam(&cams[i]));
+    DeviceGuard g(ctx->device);
+    cudaEvent_t a, b;
+    DSG_CUDA_CHECK(cudaEventCreate(&a));
+    DSG_CUDA_CHECK(cudaEventCreate(&b));
+    DSG_CUDA_CHECK(cudaEventRecord(a, ctx->stream));
+    for (int32_t r = 0; r < repeats; ++r)
+      for (const CamDev& c : cv) forward(ctx, model->m, c, rd);
+    DSG_CUDA_CHECK(cudaEventRecord(b, ctx->stream));
+    DSG_CUDA_CHECK(cudaEventSynchronize(b));
+    float t;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    *ms = t;
+  });
+}
+
+int dsg_host_register(void* ptr, int64_t bytes) {
+  return guarded([&] { DSG_CUDA_CHECK(cudaHostRegister(ptr, (size_t)bytes, cudaHostRegisterDefault)); });
+}
+
+int dsg_host_unregister(void* ptr) {
+  return guarded([&] { DSG_CUDA_CHECK(cudaHostUnregister(ptr)); });
+}
+
 int dsg_last_timing(dsg_ctx ctx, double* total_ms, double* stage_ms) {
   return guarded([&] {
     if (total_ms) *total_ms = ctx->last_total_ms;
     if (stage_ms)
-      for (int s = 0; s < 6; ++s) stage_ms[s] = ctx->last_stage_ms[s];
+      for (int s = 0; s < StageTimer::kStages; ++s) stage_ms[s] = ctx->last_stage_ms[s];
   });
 }
 

@@ -141,7 +141,10 @@ inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
-               const RenderDev& rd, cudaStream_t st) {
+               const RenderDev& rd, cudaStream_t st, StageTimer* timer) {
+  StageTimer none;
+  StageTimer& tm = timer ? *timer : none;
+  tm.mark(0, st);
   f.n = n;
   f.tiles = (int64_t)cam.tiles_x * cam.tiles_y;
   f.rec.ensure(3 * (size_t)std::max<int64_t>(n, 1));
@@ -175,7 +178,9 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     a.vis_idx = f.vis_idx.get();
     a.vis_count = f.counters.get();
     k_preprocess<<<blocks(n, 256), 256, 0, st>>>(a);
+    count_launch();
     DSG_CUDA_CHECK(cudaGetLastError());
+    tm.mark(1, st);
     uint32_t nv = 0;
     DSG_CUDA_CHECK(cudaMemcpyAsync(&nv, f.counters.get(), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -189,10 +194,13 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   uint32_t* skey = alt ? f.vis_key2.get() : f.vis_key.get();
   uint32_t* sidx = alt ? f.vis_idx2.get() : f.vis_idx.get();
   k_depth_fixup<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get());
+  count_launch();
+  tm.mark(2, st);
   f.sorted_idx = sidx;
   // per-splat tile counts in depth order, exclusive scan -> duplicate slots
   uint32_t* cnt = alt ? f.vis_key.get() : f.vis_key2.get();  // free buffer
   k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+  count_launch();
   exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
   uint32_t nd = 0;
   DSG_CUDA_CHECK(cudaMemcpyAsync(&nd, f.offs.get() + nv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
@@ -204,6 +212,8 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.dup_val2.ensure(std::max<uint32_t>(nd, 1));
   k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(), cam.tiles_x,
                                                f.tile_key.get(), f.dup_val.get(), f.dup_base.get());
+                                               count_launch();
+  tm.mark(3, st);
   int tile_bits = 1;
   while ((int64_t(1) << tile_bits) < f.tiles) ++tile_bits;
   bool alt2 = radix_sort_pairs<uint32_t>(f.tile_key.get(), f.dup_val.get(), f.tile_key2.get(),
@@ -211,7 +221,9 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
   f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
   k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get());
+  count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
+  tm.mark(4, st);
 }
 
 }  // namespace dsg

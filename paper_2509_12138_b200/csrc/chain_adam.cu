@@ -256,12 +256,14 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
 void chain_3d(const ChainArgs& a, cudaStream_t st) {
   if (a.n == 0) return;
   k_chain<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a);
+  count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
 
 void adam_update(const AdamArgs& a, cudaStream_t st) {
   if (a.n == 0) return;
   k_adam<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a);
+  count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -23,6 +23,8 @@ enum Code {
   kMissingBaseline, kInvalidArgument
 };
 [[noreturn]] void fail(int code, const std::string& msg);
+// Counts this library's kernel launches (reported by bench.py as gpu_launches).
+void count_launch(int n = 1);
 
 // Growable raw device allocation (never shrinks; contents not preserved).
 template <class T>

@@ -277,8 +277,11 @@ void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, 
   a.loss_out = f.loss_out.get();
   a.nblocks = nblocks;
   k_ssim_stats<<<grid, kB * kB, 0, st>>>(a);
+  count_launch();
   k_loss_grad<<<grid, kB * kB, 0, st>>>(a);
+  count_launch();
   k_loss_final<<<1, 256, 0, st>>>(a);
+  count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
 

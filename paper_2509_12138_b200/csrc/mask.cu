@@ -44,6 +44,7 @@ void render_mask_dev(const double* pts, int64_t n, const CamDev& cam, double rad
   if (n <= 0) return;
   k_render_mask<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(pts, n, cam, radius, radius * radius,
                                                               mask);
+                                                              count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
 

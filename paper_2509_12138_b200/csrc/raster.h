@@ -90,8 +90,20 @@ struct AdamArgs {
   int accumulate_stats;
 };
 
+// Optional per-stage CUDA-event timer (profiling mode of dsg_train).
+// Marks: 0 start, 1 preprocess, 2 depth sort, 3 scan+duplicate, 4 tile
+// sort+ranges, 5 blend fwd, 6 loss, 7 blend bwd, 8 chain, 9 adam.
+struct StageTimer {
+  static constexpr int kStages = 9;
+  cudaEvent_t ev[kStages + 1] = {};
+  bool on = false;
+  void mark(int i, cudaStream_t st) {
+    if (on) DSG_CUDA_CHECK(cudaEventRecord(ev[i], st));
+  }
+};
+
 void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
-               const RenderDev& rd, cudaStream_t st);
+               const RenderDev& rd, cudaStream_t st, StageTimer* timer = nullptr);
 void blend_forward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,
                    const RenderDev& rd, cudaStream_t st);
 void blend_backward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,
@@ -103,6 +115,15 @@ void adam_update(const AdamArgs& a, cudaStream_t st);
 // K11: stamp render_mask discs of `radius` px into a zeroed byte mask.
 void render_mask_dev(const double* pts, int64_t n, const CamDev& cam, double radius,
                      uint8_t* mask, cudaStream_t st);
+// knn_mean_distances (seed.hpp:16-35): exact grid search; host_pts is the
+// host copy of pts (bounds), out on device.
+void knn_mean_dev(const double* host_pts, const double* pts, int64_t n, int k, double* out,
+                  SortScratch& ss, cudaStream_t st);
+// seed_gaussians / ground_truth_model params (seed.hpp:49-94): log-scale from
+// scale[i] (or fixed_ls when scale is null), identity rotation.
+void seed_params_dev(const double* pts, const double* colors, const double* scale, int64_t n,
+                     double fixed_ls, double opacity_logit, float* params, int64_t pitch,
+                     cudaStream_t st);
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
                      double lambda, cudaStream_t st);
 

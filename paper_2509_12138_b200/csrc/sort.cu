@@ -252,8 +252,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratc
   int64_t nb = (n + kScanTile - 1) / kScanTile;
   uint32_t* sums = s.block_sums.ensure(nb + 1);
   k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
+  count_launch();
   k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
+  count_launch();
   k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums);
+  count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -272,6 +275,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
   DSG_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * passes, st));
   int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
   k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, hist);
+  count_launch();
   // Which digits actually vary? (a single populated bin = identity pass)
   s.host_hist.resize((size_t)passes * kRadix);
   DSG_CUDA_CHECK(cudaMemcpyAsync(s.host_hist.data(), hist, sizeof(uint32_t) * passes * kRadix,
@@ -282,6 +286,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
     for (int d = 0; d < kRadix; ++d)
       if (s.host_hist[(size_t)p * kRadix + d] == (uint32_t)n) trivial[p] = true;
   k_hist_scan<<<passes, kRadix, 0, st>>>(hist);
+  count_launch();
   const size_t smem = sizeof(OnesweepSmem<K>);
   DSG_CUDA_CHECK(cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
@@ -295,6 +300,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
     k_onesweep<K><<<(unsigned)parts, kSortThreads, smem, st>>>(
         ki, vi, ko, vo, n, begin_bit + kRadixBits * p, hist + (size_t)p * kRadix,
         status + (size_t)p * parts * kRadix, counters + p);
+        count_launch();
     in_alt = !in_alt;
   }
   DSG_CUDA_CHECK(cudaGetLastError());
