@@ -21,7 +21,8 @@ from .types import (PARAMS, AdamConfig, Camera, DsplatError, ErrorCode, Gradient
                     TrainView)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdsg.so")
+# DSG_LIB selects an alternative in-tree build (A/B kernel experiments only).
+LIB_PATH = os.environ.get("DSG_LIB") or os.path.join(HERE, "libdsg.so")
 
 
 class dsg_camera(C.Structure):

@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
         r[1] = make_float4((float)ixx, (float)ixy, (float)iyy, (float)op);
         r[2] = make_float4((float)p[11], (float)p[12], (float)p[13], (float)kappa);
         int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
-        a.trect[i] = make_int4(tx0, ty0, tx1, ty1);
+        a.trect[i] = make_int4(x0, y0, x1, y1);  // pixel rect; tile rect = rect / kTile
         count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         a.depth[i] = pr.depth;
         depth_f = (float)pr.depth;
@@ -118,7 +118,8 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
   uint32_t i = vis_idx[s];
   uint32_t o = offs[s];
   dup_base[i] = o;
-  int4 r = trect[i];
+  const int4 pr = trect[i];
+  const int4 r = make_int4(pr.x / kTile, pr.y / kTile, pr.z / kTile, pr.w / kTile);
   for (int ty = r.y; ty <= r.w; ++ty)
     for (int tx = r.x; tx <= r.z; ++tx) {
       tile_key[o] = (uint32_t)(ty * tiles_x + tx);
@@ -128,6 +129,27 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
 }
 
 // K4: [start, end) of every tile in the sorted duplicate list.
+// Per sorted entry, the 8x4 sub-tiles of its tile that its pixel rect
+// (widened by one pixel) touches: bit (sy*2 + sx). Lets each blend warp skip
+// entries that cannot reach its pixels from one coalesced byte read.
+__global__ void k_entry_masks(const uint32_t* __restrict__ tile_key,
+                              const uint32_t* __restrict__ val, const int4* __restrict__ prect,
+                              int64_t nd, int tiles_x, uint8_t* __restrict__ mask) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nd) return;
+  const uint32_t t = tile_key[e];
+  const int4 pr = prect[val[e]];
+  const int ox = (int)(t % (uint32_t)tiles_x) * kTile, oy = (int)(t / (uint32_t)tiles_x) * kTile;
+  const int x0 = pr.x - 1 - ox, x1 = pr.z + 1 - ox, y0 = pr.y - 1 - oy, y1 = pr.w + 1 - oy;
+  uint32_t m = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    const int cx0 = (w & 1) * 8, cy0 = (w >> 1) * 4;
+    if (x0 <= cx0 + 7 && x1 >= cx0 && y0 <= cy0 + 3 && y1 >= cy0) m |= 1u << w;
+  }
+  mask[e] = (uint8_t)m;
+}
+
 __global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd, uint2* ranges) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nd) return;
@@ -221,6 +243,10 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
   f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
   k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get());
+  count_launch();
+  f.emask.ensure(std::max<uint32_t>(nd, 1));
+  k_entry_masks<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, f.sorted_val, f.trect.get(), nd,
+                                                 cam.tiles_x, f.emask.get());
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
   tm.mark(4, st);

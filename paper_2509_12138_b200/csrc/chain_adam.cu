@@ -52,13 +52,21 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   bool touched = false;
   const uint32_t cnt = a.tcount[i];
   if (cnt) {
-    const float2* pp = reinterpret_cast<const float2*>(a.partials + (size_t)a.dup_base[i] * 10);
-    for (uint32_t k = 0; k < cnt; ++k, pp += 5) {
-      float2 v0 = pp[0], v1 = pp[1], v2 = pp[2], v3 = pp[3], v4 = pp[4];
-      if (v4.y == 0.f) continue;
+    // fold (duplicate, sub-tile) slots in fixed tile-then-sub-tile order
+    const uint32_t base = a.dup_base[i];
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const uint32_t d = base + k;
+      uint32_t m = (a.tmask[d >> 2] >> (8 * (d & 3))) & 0xffu;
+      if (!m) continue;
       touched = true;
-      acc[0] += v0.x; acc[1] += v0.y; acc[2] += v1.x; acc[3] += v1.y; acc[4] += v2.x;
-      acc[5] += v2.y; acc[6] += v3.x; acc[7] += v3.y; acc[8] += v4.x;
+      const float* pp = a.partials + (size_t)d * 8 * 9;
+      while (m) {
+        const int w = __ffs(m) - 1;
+        m &= m - 1;
+        const float* q = pp + w * 9;
+#pragma unroll
+        for (int v = 0; v < 9; ++v) acc[v] += q[v];
+      }
     }
   }
   float* G = a.grads;

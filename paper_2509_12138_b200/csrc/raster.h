@@ -10,7 +10,7 @@ struct PreprocessArgs {
   CamDev cam;
   RenderDev rd;
   float4* rec;          // [n][3] blend payload (model order)
-  int4* trect;          // [n] tile rect (tx0, ty0, tx1, ty1)
+  int4* trect;          // [n] pixel rect (x0, y0, x1, y1), render.hpp:71-81
   uint32_t* tcount;     // [n] overlapped tiles (0 = culled)
   double* depth;        // [n] camera-space depth (fp64)
   uint32_t* vis_key;    // [n] compacted fp32 depth bits
@@ -36,13 +36,18 @@ struct Frame {
   uint32_t* sorted_tile = nullptr;
   uint32_t* sorted_val = nullptr;
   DevBuf<uint2> ranges;
+  DevBuf<uint8_t> emask;      // per sorted entry: touched 8x4 sub-tiles of its tile
   DevBuf<uint32_t> counters;
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL;
   DevBuf<uint32_t> last;
   DevBuf<int32_t> ncontrib;
   // backward partials [n_dup][10]
-  DevBuf<float> partials;
+  DevBuf<float> partials;     // [n_dup][8 sub-tiles][9] screen gradients
+  DevBuf<uint32_t> tmask;     // 8-bit touched-sub-tile mask per duplicate, 4 per word
+  // device copy of the blend kernels' guard-band context (read by the rare
+  // fp64 path through a pointer, so it never lands on the thread stack)
+  DevBuf<uint8_t> evalctx;
   // loss scratch
   DevBuf<double> ssim_pqr, loss_parts;
   DevBuf<uint32_t> loss_counts;
@@ -69,6 +74,7 @@ struct ChainArgs {
   const uint32_t* tcount;
   const uint32_t* dup_base;
   const float* partials;
+  const uint32_t* tmask;
   float* grads;     // [14][pitch]
   float* dmean;     // [2][pitch]
   int32_t* touch;   // [n]
