@@ -56,6 +56,10 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
         a.trect[i] = make_int4(x0, y0, x1, y1);  // pixel rect; tile rect = rect / kTile
         count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
         a.depth[i] = pr.depth;
+        double2* ex = a.exact + 3 * i;
+        ex[0] = make_double2(pr.mx, pr.my);
+        ex[1] = make_double2(ixx, ixy);
+        ex[2] = make_double2(iyy, op);
         depth_f = (float)pr.depth;
         vis = true;
       }
@@ -173,6 +177,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.trect.ensure(std::max<int64_t>(n, 1));
   f.tcount.ensure(std::max<int64_t>(n, 1));
   f.depth.ensure(std::max<int64_t>(n, 1));
+  f.exact.ensure(3 * (size_t)std::max<int64_t>(n, 1));
   f.dup_base.ensure(std::max<int64_t>(n, 1));
   f.vis_key.ensure(std::max<int64_t>(n, 1));
   f.vis_idx.ensure(std::max<int64_t>(n, 1));
@@ -196,6 +201,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     a.trect = f.trect.get();
     a.tcount = f.tcount.get();
     a.depth = f.depth.get();
+    a.exact = f.exact.get();
     a.vis_key = f.vis_key.get();
     a.vis_idx = f.vis_idx.get();
     a.vis_count = f.counters.get();

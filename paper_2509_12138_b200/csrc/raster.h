@@ -13,6 +13,7 @@ struct PreprocessArgs {
   int4* trect;          // [n] pixel rect (x0, y0, x1, y1), render.hpp:71-81
   uint32_t* tcount;     // [n] overlapped tiles (0 = culled)
   double* depth;        // [n] camera-space depth (fp64)
+  double2* exact;       // [n][3] fp64 (mx,my) (ixx,ixy) (iyy,op) for the guard band
   uint32_t* vis_key;    // [n] compacted fp32 depth bits
   uint32_t* vis_idx;    // [n] compacted gaussian index
   uint32_t* vis_count;
@@ -28,6 +29,7 @@ struct Frame {
   DevBuf<int4> trect;
   DevBuf<uint32_t> tcount, dup_base;
   DevBuf<double> depth;
+  DevBuf<double2> exact;     // [n][3] fp64 mean2d, conic, opacity
   // visible set, depth-sorted
   DevBuf<uint32_t> vis_key, vis_idx, vis_key2, vis_idx2, offs;
   uint32_t* sorted_idx = nullptr;

@@ -29,6 +29,8 @@ cams = [rig[i] for i in (5, 60, 117, 200, 251, 333, 401)]
 gt = api.ground_truth_model(pts, cols, nn, 0.97, ctx=ctx)
 views = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), cams, pts, True, 2.0, 2.0)
 seeds = api.seed_gaussians(pts, cols, 3, ctx=ctx)
+api.train_device(seeds, views, TrainConfig(iterations=3, seed=1))  # warm-up: allocations
+seeds.upload(seeds.download())
 ctx.set_profiling(True)
 api.train_device(seeds, views, TrainConfig(iterations=args.iters, seed=1))
 tot, st = ctx.last_timing()
