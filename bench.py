@@ -105,7 +105,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thr = threading.Thread(target=self._read, daemon=True)
             self.thr.start()
@@ -204,20 +204,45 @@ def train_config(args, rank: int, iterations: int) -> TrainConfig:
     return TrainConfig(iterations=iterations, seed=1 + rank)
 
 
-def roofline_for(stage: str, ms: float, n: int, npix: int, n_dup: int, peak: float):
-    """Algorithmic bytes per launch for the HBM-bound kernels."""
-    per = {
-        "adam": 412.0 * n,              # p,g,m,v read 224 B, p,m,v write 168 B, stats 20 B
-        "preprocess": 140.0 * n,        # params 56 B read, payload 84 B write
-        "chain": (56.0 + 56.0 + 12.0) * n + 40.0 * n_dup,
+KERNEL_OF_STAGE = {"preprocess": "k_preprocess", "depth_sort": "k_onesweep (depth)",
+                   "scan_duplicate": "k_duplicate", "tile_sort_ranges": "k_onesweep (tile)",
+                   "blend_fwd": "k_blend_fwd", "loss": "k_ssim_stats+k_loss_grad",
+                   "blend_bwd": "k_blend_bwd", "chain": "k_chain", "adam": "k_adam"}
+
+
+def algorithmic_bytes(stage: str, n: int, nv: int, npix: int, n_dup: int) -> float:
+    """Minimal HBM bytes one launch must move."""
+    return {
+        "preprocess": 56.0 * n + 4.0 * n + 104.0 * nv,     # params in; count; payload+rect+depth+key out
+        "depth_sort": 4 * 16.0 * nv + 8.0 * nv,            # 4 passes x (key,val) r+w, 1 histogram read
+        "scan_duplicate": 12.0 * nv + 12.0 * n_dup,        # counts, scan, (tile,val) pairs out
+        "tile_sort_ranges": 2 * 16.0 * n_dup + 9.0 * n_dup,  # 2 passes, ranges + sub-tile masks
+        "blend_fwd": 5.0 * n_dup + 48.0 * n_dup + 20.0 * npix,   # list + payload per entry, pixel out
         "loss": 37.0 * npix,
-    }
-    if stage not in per or ms <= 0:
-        return None
-    b = per[stage]
-    gbs = b / (ms * 1e-3) / 1e9
-    return {"bound": "hbm", "kernel": stage, "achieved": round(gbs, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(gbs / peak, 4), "bytes_per_launch": b, "traffic": None}
+        "blend_bwd": 5.0 * n_dup + 68.0 * n_dup + 20.0 * npix + 36.0 * n_dup,  # + >=1 partial/entry
+        "chain": 112.0 * n + 36.0 * n_dup + 4.0 * n_dup,   # params+grads, partials, masks
+        "adam": 412.0 * n,                                  # p,g,m,v in; p,m,v out; stats
+    }[stage]
+
+
+def roofline(stage_ms, n, nv, npix, n_dup, peak, peak_kind):
+    rows = {}
+    for st, ms in stage_ms.items():
+        if ms <= 0:
+            continue
+        b = algorithmic_bytes(st, n, nv, npix, n_dup)
+        gbs = b / (ms * 1e-3) / 1e9
+        rows[st] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    dom = max(stage_ms, key=stage_ms.get)
+    d = rows[dom]
+    out = {"bound": "hbm", "kernel": KERNEL_OF_STAGE[dom], "achieved": d["GB/s"], "peak": peak,
+           "unit": "GB/s", "frac": d["frac"],
+           "bytes_per_launch": algorithmic_bytes(dom, n, nv, npix, n_dup), "traffic": None,
+           "peak_kind": peak_kind, "per_stage": rows}
+    if dom in ("blend_fwd", "blend_bwd"):
+        out["note"] = ("dominant kernel is the per-pixel blend: FP32/issue- and latency-bound, "
+                       "not HBM-bound; see profiles/ for issue-slot and stall data")
+    return out
 
 
 def load_peak():
@@ -268,7 +293,8 @@ def run_ours(args, dist: Dist):
     prof_total, stages = ctx.last_timing()
     ctx.set_profiling(False)
     stage_ms = {s: float(v) / pk for s, v in zip(api.STAGES, stages)}
-    n_dup = api.frame_stats(ctx)["n_dup"]
+    fs = api.frame_stats(ctx)
+    n_dup, nv_vis = fs["n_dup"], fs["n_visible"]
 
     # render Mpix/s on the test views (forward only, device-timed)
     test_cams = [inp["rig"][i] for i in inp["test_idx"]]
@@ -300,14 +326,7 @@ def run_ours(args, dist: Dist):
     del out
 
     peak, peak_kind = load_peak()
-    dom = max(stage_ms, key=stage_ms.get)
-    hbm_stages = [s for s in ("adam", "preprocess", "chain", "loss") if stage_ms.get(s, 0) > 0]
-    dom_hbm = max(hbm_stages, key=lambda s: stage_ms[s]) if hbm_stages else None
-    roof = roofline_for(dom_hbm, stage_ms[dom_hbm], n, npix, n_dup, peak) if dom_hbm else None
-    if roof:
-        roof["peak_kind"] = peak_kind
-        roof["note"] = (f"dominant HBM-bound kernel; step-dominant stage is {dom} "
-                        f"({stage_ms[dom]:.3f} ms of {prof_total / pk:.3f} ms, FP32/issue-bound blend)")
+    roof = roofline(stage_ms, n, nv_vis, npix, n_dup, peak, peak_kind)
 
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
@@ -376,6 +395,9 @@ def run_reference(args, dist: Dist):
     seeds_host = inp["seeds"].download()
     views = inp["views"]
     cores = os.cpu_count() or 1
+    # each CPU step is ~15-60 s: bound the whole run to a few minutes
+    args.steps = min(args.steps, 4)
+    args.warmup = min(args.warmup, 1)
     order = api.view_order(1, len(views), args.warmup + args.steps)
     for it in range(args.warmup):
         tv = views.download(int(order[it]))
@@ -412,7 +434,7 @@ def _single():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=list(scenes.SIZES), default="kingsnake")
