@@ -93,6 +93,10 @@ int dsg_model_destroy(dsg_model model);
 /* Upload a SplatModel (gaussian.hpp:41-54); resets Adam moments and stats. */
 int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t n,
                      int64_t iteration, int32_t origin_partition);
+/* Overwrite the parameters of an existing model of the same size, keeping
+ * its Adam moments and statistics (host-side AdamState mirrors). */
+int dsg_model_set_params(dsg_ctx ctx, dsg_model model, const double* params, int64_t n,
+                         int64_t iteration);
 int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t capacity,
                        int64_t* n, int64_t* iteration, int32_t* origin_partition);
 int dsg_model_info(dsg_model model, int64_t* n, int64_t* iteration, int64_t* adam_step);

@@ -420,6 +420,24 @@ int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t
   });
 }
 
+int dsg_model_set_params(dsg_ctx ctx, dsg_model model, const double* params, int64_t n,
+                         int64_t iteration) {
+  return guarded([&] {
+    ModelDev& m = model->m;
+    if (n != m.n) fail(kMismatchedCounts, "model size differs from the device model");
+    DeviceGuard g(ctx->device);
+    m.iteration = iteration;
+    if (n > 0) {
+      double* st = ctx->stage_d.ensure(kParams * n);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(st, params, sizeof(double) * kParams * n, cudaMemcpyHostToDevice,
+                                     ctx->stream));
+      k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
+      count_launch();
+    }
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t capacity,
                        int64_t* n, int64_t* iteration, int32_t* origin_partition) {
   return guarded([&] {

@@ -1,0 +1,127 @@
+// Drop-in parity: the reference C++ API (CPU, /root/reference headers) against
+// dsplat::b200 (include/dsplat_b200/dsplat_b200.hpp -> libdsg.so on the B200),
+// called with the SAME reference types. Exit code = number of failures.
+// Built here by tests/cpp/Makefile (needs the reference headers); the binary
+// travels to the GPU box and is run by tests/test_cpp_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "dsplat/backward.hpp"
+#include "dsplat/trainer.hpp"
+#include "dsplat_b200/dsplat_b200.hpp"
+
+using namespace dsplat;
+
+static int failures = 0;
+#define EXPECT(cond, ...)                      \
+  do {                                         \
+    if (!(cond)) {                             \
+      ++failures;                              \
+      std::printf("FAIL %s: ", #cond);         \
+      std::printf(__VA_ARGS__);                \
+      std::printf("\n");                       \
+    }                                          \
+  } while (0)
+
+static float f32(double v) { return static_cast<float>(v); }
+
+static SplatModel scene(uint64_t seed, int n, double scale_mul) {
+  Rng rng(seed);
+  SplatModel m;
+  for (int i = 0; i < n; ++i) {
+    Gaussian3D g;
+    g.mu = {f32(rng.uniform(-0.5, 0.5)), f32(rng.uniform(-0.5, 0.5)), f32(rng.uniform(-0.4, 0.4))};
+    double s = rng.uniform(0.08, 0.35) * scale_mul;
+    g.log_scale = {f32(std::log(s * rng.uniform(0.6, 1.6))), f32(std::log(s * rng.uniform(0.6, 1.6))),
+                   f32(std::log(s * rng.uniform(0.6, 1.6)))};
+    Quat q{rng.normal(), rng.normal(), rng.normal(), rng.normal()};
+    q = q.normalized();
+    g.rot = {f32(q.w), f32(q.x), f32(q.y), f32(q.z)};
+    g.opacity_logit = f32(rng.uniform(-1.0, 1.5));
+    g.color = {f32(rng.uniform(0.2, 0.8)), f32(rng.uniform(0.2, 0.8)), f32(rng.uniform(0.2, 0.8))};
+    m.gaussians.push_back(g);
+  }
+  return m;
+}
+
+static Camera cam(int res) {
+  Camera c;
+  c.position = {0.2, 0.1, -3};
+  c.target = {0, 0, 0};
+  c.width = c.height = res;
+  c.near = 0.1;
+  c.far = 50;
+  return c;
+}
+
+int main() {
+  RenderConfig cfg;
+  for (int k = 0; k < 4; ++k) {
+    SplatModel m = scene(100 + k, 40 + 30 * k, k == 3 ? 0.2 : 1.0);
+    Camera c = cam(48 + 16 * k);
+    RenderOutput a = render(m, c, cfg);
+    RenderOutput b = b200::render(m, c, cfg);
+    double err = 0;
+    for (size_t i = 0; i < a.color.pixels.size(); ++i)
+      err = std::max(err, std::abs(a.color.pixels[i] - b.color.pixels[i]));
+    EXPECT(err <= 1e-3, "render %d max err %g", k, err);
+    EXPECT(a.splat_order == b.splat_order, "render %d splat order", k);
+
+    // masked loss + backward
+    TrainView v;
+    v.cam = c;
+    v.ground_truth = render(scene(200 + k, 40, 1.0), c, cfg).color;
+    v.mask = Image(c.width, c.height, 1, 1.0);
+    LossResult la = masked_loss(a.color, v, 0.2);
+    LossResult lb = b200::masked_loss(a.color, v, 0.2);
+    EXPECT(std::abs(la.loss - lb.loss) <= 1e-6 * std::abs(la.loss), "loss %d %g vs %g", k, la.loss,
+           lb.loss);
+    GradientBuffer ga = backward(m, c, cfg, a, la.dL_dpixels);
+    GradientBuffer gb = b200::backward(m, c, cfg, b, la.dL_dpixels);
+    double scale = 0, gerr = 0;
+    for (size_t i = 0; i < m.size(); ++i) {
+      scale = std::max(scale, ga.d_mu[i].norm());
+      gerr = std::max(gerr, (ga.d_mu[i] - gb.d_mu[i]).norm());
+      EXPECT(ga.touch_count[i] == gb.touch_count[i], "touch %d/%zu", k, i);
+    }
+    EXPECT(gerr <= 1e-3 * scale, "backward %d d_mu err %g scale %g", k, gerr, scale);
+  }
+  // errors keep the reference's codes and text
+  {
+    SplatModel m = scene(5, 3, 1.0);
+    RenderOutput out = b200::render(m, cam(32), cfg);
+    m.iteration += 1;
+    try {
+      b200::backward(m, cam(32), cfg, out, Image(32, 32, 3));
+      EXPECT(false, "StaleForward not thrown");
+    } catch (const Error& e) {
+      EXPECT(std::string(e.what()).find("StaleForward") == 0, "what() = %s", e.what());
+    }
+    try {
+      b200::train_partition(m, {}, TrainConfig{});
+      EXPECT(false, "NoViews not thrown");
+    } catch (const Error& e) {
+      EXPECT(e.code() == ErrorCode::NoViews, "code");
+    }
+  }
+  // a short training run tracks the reference
+  {
+    Camera c = cam(40);
+    SplatModel init = scene(23, 12, 1.0);
+    TrainView v;
+    v.cam = c;
+    v.ground_truth = render(scene(24, 12, 1.0), c, cfg).color;
+    v.mask = Image(40, 40, 1, 1.0);
+    TrainConfig tc;
+    tc.iterations = 20;
+    tc.seed = 9;
+    TrainResult ra = train_partition_full(init, {v}, tc);
+    TrainResult rb = b200::train_partition_full(init, {v}, tc);
+    EXPECT(std::abs(ra.final_loss - rb.final_loss) <= 2e-3 * ra.final_loss, "train loss %g vs %g",
+           ra.final_loss, rb.final_loss);
+    EXPECT(rb.model.iteration == init.iteration + 20, "iteration %ld", (long)rb.model.iteration);
+  }
+  std::printf("dropin_parity: %d failure(s)\n", failures);
+  return failures;
+}
