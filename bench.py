@@ -149,8 +149,7 @@ def build_partition_inputs(args, dist: Dist, ctx):
     n_total = args.n_per_gpu * dist.world
     t0 = time.time()
     if args.workload == "kingsnake":
-        pts, cols, _ = scenes.kingsnake(n_total, seed=1, turns=6.0 * dist.world,
-                                        length=1.0 * dist.world)
+        pts, cols, _ = scenes.kingsnake(n_total, seed=1, turns=6.0 * dist.world)
     else:
         pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
     nn = api.median_nn_spacing(pts, ctx=ctx)          # resolve_auto_values (runtime.hpp:73-77)

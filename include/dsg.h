@@ -189,6 +189,37 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
               int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
               double* loss_trace);
 
+/* ---- partition / merge / multi-GPU (partition.hpp) --------------- */
+/* partition_cloud (partition.hpp:42-104) on the device: positions [n][3];
+ * cut_lo/cut_hi [nparts], owned_box [nparts][6] (lo xyz, hi xyz), per-part
+ * counts, and owned/ghost index lists concatenated in partition order
+ * (capacity cap each), every list in ascending point index. */
+int dsg_partition(dsg_ctx ctx, const double* positions, int64_t n, int32_t nparts, double margin,
+                  int32_t* axis, double* cut_lo, double* cut_hi, double* owned_box,
+                  int64_t* owned_count, int64_t* ghost_count, uint32_t* owned_idx,
+                  uint32_t* ghost_idx, int64_t cap);
+/* merge_models (partition.hpp:109-126) of device models in one process:
+ * keep splats whose mu[axis] is in [cut_lo[k], cut_hi[k]), in (k, index)
+ * order; out.iteration = max. */
+int dsg_merge_models(dsg_ctx ctx, const dsg_model* models, int32_t nparts, int32_t axis,
+                     const double* cut_lo, const double* cut_hi, dsg_model out);
+typedef struct dsg_comm_s* dsg_comm;
+/* NCCL communicator over the ranks' GPUs (one rank per process/GPU). */
+int dsg_comm_unique_id(uint8_t* out128);
+int dsg_comm_create(dsg_ctx ctx, const uint8_t* id128, int32_t nranks, int32_t rank,
+                    dsg_comm* out);
+int dsg_comm_destroy(dsg_comm comm);
+/* Distributed merge: trim this rank's partition model to its owned slab,
+ * all-gather survivor counts, broadcast survivors so every rank holds the
+ * merged model in (partition = rank, index) order. *ms = device time. */
+int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
+                        double cut_hi, dsg_model merged, int64_t* n_merged, double* ms);
+/* Tile-parallel render (comm may be NULL): rank r bins and blends tile-row
+ * band r of the replicated model; bands are gathered to rank 0, which
+ * receives rgb [h][w][3] (may be NULL). *ms = device time incl. the gather. */
+int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const dsg_camera* cam,
+                           const dsg_render_config* cfg, double* rgb, double* ms);
+
 /* Number of this library's kernel launches so far (process-wide). */
 int64_t dsg_launch_count(void);
 /* Visible splats and tile duplicates of the last view binned on ctx. */

@@ -507,3 +507,88 @@ def pinned(a: np.ndarray) -> np.ndarray:
     a = np.ascontiguousarray(a)
     _check(lib().dsg_host_register(C.c_void_p(a.ctypes.data), C.c_int64(a.nbytes)))
     return a
+
+
+# ---- partition / merge / multi-GPU ---------------------------------------------
+def partition_cloud(positions, n: int, ghost_margin: float, ctx: Context = None):
+    """partition_cloud (partition.hpp:42-104) on the device (fp64, exact)."""
+    from .types import Partition
+    ctx = ctx or default_context()
+    pts = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+    npts = pts.shape[0]
+    k = max(n, 1)
+    ax = C.c_int32()
+    lo, hi, box = np.zeros(k), np.zeros(k), np.zeros((k, 6))
+    oc, gc = np.zeros(k, np.int64), np.zeros(k, np.int64)
+    cap = max(1, npts * k)
+    oi, gi = np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
+    _check(lib().dsg_partition(ctx.h, _p(pts), C.c_int64(npts), C.c_int32(n),
+                               C.c_double(ghost_margin), C.byref(ax), _p(lo), _p(hi), _p(box),
+                               _p(oc, C.c_int64), _p(gc, C.c_int64), _p(oi, C.c_uint32),
+                               _p(gi, C.c_uint32), C.c_int64(cap)))
+    parts, o, g = [], 0, 0
+    for j in range(n):
+        parts.append(Partition(j, ax.value, float(lo[j]), float(hi[j]), box[j].reshape(2, 3).copy(),
+                               ghost_margin, oi[o:o + oc[j]].copy(), gi[g:g + gc[j]].copy()))
+        o += oc[j]
+        g += gc[j]
+    return parts
+
+
+def merge_models(models, partitions, ctx: Context = None) -> DeviceModel:
+    """merge_models (partition.hpp:109-126) over device models, one process."""
+    ctx = ctx or default_context()
+    if len(models) != len(partitions):
+        raise DsplatError(ErrorCode.MismatchedCounts, "one model per partition required")
+    dms = [m if isinstance(m, DeviceModel) else DeviceModel(ctx, m) for m in models]
+    arr = (C.c_void_p * len(dms))(*[d.h.value for d in dms])
+    lo = np.array([p.cut_lo for p in partitions])
+    hi = np.array([p.cut_hi for p in partitions])
+    out = DeviceModel(ctx)
+    _check(lib().dsg_merge_models(ctx.h, arr, C.c_int32(len(dms)),
+                                  C.c_int32(partitions[0].cut_axis), _p(lo), _p(hi), out.h))
+    return out
+
+
+class Comm:
+    """NCCL communicator (dsg_comm); the unique id travels over any side channel."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        _check(lib().dsg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, ctx: Context, uid: bytes, nranks: int, rank: int):
+        self.ctx = ctx
+        self.h = C.c_void_p()
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().dsg_comm_create(ctx.h, buf, C.c_int32(nranks), C.c_int32(rank),
+                                     C.byref(self.h)))
+        self.nranks, self.rank = nranks, rank
+
+    def close(self):
+        if self.h:
+            lib().dsg_comm_destroy(self.h)
+            self.h = C.c_void_p()
+
+
+def merge_allgather(comm: Comm, local: DeviceModel, partition) -> tuple:
+    """Ghost-trim this rank's partition and all-gather the merged model."""
+    merged = DeviceModel(comm.ctx)
+    n, ms = C.c_int64(), C.c_double()
+    _check(lib().dsg_merge_allgather(comm.ctx.h, comm.h, local.h, C.c_int32(partition.cut_axis),
+                                     C.c_double(partition.cut_lo), C.c_double(partition.cut_hi),
+                                     merged.h, C.byref(n), C.byref(ms)))
+    return merged, n.value, ms.value
+
+
+def render_distributed(comm, model: DeviceModel, cam: Camera, cfg: RenderConfig, want_image=True):
+    """Tile-parallel render with the bands gathered to rank 0 (comm may be None)."""
+    ctx = model.ctx
+    rgb = np.zeros((cam.height, cam.width, 3)) if want_image else None
+    ms = C.c_double()
+    _check(lib().dsg_render_distributed(ctx.h, comm.h if comm else None, model.h,
+                                        C.byref(cam_struct(cam)), C.byref(cfg_struct(cfg)),
+                                        _p(rgb), C.byref(ms)))
+    return rgb, ms.value

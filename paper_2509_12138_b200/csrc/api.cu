@@ -162,6 +162,8 @@ CamDev make_cam(const dsg_camera* c) {
   k.height = c->height;
   k.tiles_x = (c->width + kTile - 1) / kTile;
   k.tiles_y = (c->height + kTile - 1) / kTile;
+  k.band_ty0 = 0;
+  k.band_ty1 = k.tiles_y;
   return k;
 }
 
@@ -1074,6 +1076,164 @@ int dsg_host_register(void* ptr, int64_t bytes) {
 
 int dsg_host_unregister(void* ptr) {
   return guarded([&] { DSG_CUDA_CHECK(cudaHostUnregister(ptr)); });
+}
+
+int dsg_partition(dsg_ctx ctx, const double* positions, int64_t n, int32_t nparts, double margin,
+                  int32_t* axis, double* cut_lo, double* cut_hi, double* owned_box,
+                  int64_t* owned_count, int64_t* ghost_count, uint32_t* owned_idx,
+                  uint32_t* ghost_idx, int64_t cap) {
+  return guarded([&] {  // partition.hpp:42-104
+    DeviceGuard g(ctx->device);
+    PartitionResult r = partition_dev(positions, n, nparts, margin, ctx->frame.sort,
+                                      ctx->frame.scan, ctx->stream);
+    *axis = r.axis;
+    int64_t oi = 0, gi = 0;
+    for (int k = 0; k < nparts; ++k) {
+      cut_lo[k] = r.cut_lo[k];
+      cut_hi[k] = r.cut_hi[k];
+      for (int c = 0; c < 6; ++c) owned_box[6 * k + c] = r.box[6 * k + c];
+      owned_count[k] = (int64_t)r.owned[k].size();
+      ghost_count[k] = (int64_t)r.ghost[k].size();
+      for (uint32_t x : r.owned[k]) {
+        if (oi < cap) owned_idx[oi] = x;
+        ++oi;
+      }
+      for (uint32_t x : r.ghost[k]) {
+        if (gi < cap) ghost_idx[gi] = x;
+        ++gi;
+      }
+    }
+    if (oi > cap || gi > cap) fail(kInvalidArgument, "index capacity too small");
+  });
+}
+
+int dsg_merge_models(dsg_ctx ctx, const dsg_model* models, int32_t nparts, int32_t axis,
+                     const double* cut_lo, const double* cut_hi, dsg_model out) {
+  return guarded([&] {  // merge_models (partition.hpp:109-126), single process
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    std::vector<int64_t> cnt(nparts);
+    int64_t total = 0, it = 0;
+    for (int k = 0; k < nparts; ++k) {
+      const ModelDev& m = models[k]->m;
+      cnt[k] = merge_compact_dev(m.params.get(), m.cap, m.n, axis, cut_lo[k], cut_hi[k], nullptr,
+                                 0, 0, ctx->frame.scan, st);
+      total += cnt[k];
+      it = std::max(it, m.iteration);
+    }
+    ModelDev& o = out->m;
+    o.reserve(std::max<int64_t>(total, 1));
+    o.n = total;
+    o.iteration = it;
+    o.origin_partition = -1;
+    int64_t off = 0;
+    for (int k = 0; k < nparts; ++k) {
+      const ModelDev& m = models[k]->m;
+      merge_compact_dev(m.params.get(), m.cap, m.n, axis, cut_lo[k], cut_hi[k], o.params.get(),
+                        o.cap, off, ctx->frame.scan, st);
+      off += cnt[k];
+    }
+    reset_optimizer(ctx, o);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+struct dsg_comm_s {
+  void* nccl = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+int dsg_comm_unique_id(uint8_t* out128) {
+  return guarded([&] { nccl_unique_id(out128); });
+}
+
+int dsg_comm_create(dsg_ctx ctx, const uint8_t* id128, int32_t nranks, int32_t rank,
+                    dsg_comm* out) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    auto* c = new dsg_comm_s();
+    c->nranks = nranks;
+    c->rank = rank;
+    c->nccl = nccl_comm_init(id128, nranks, rank);
+    *out = c;
+  });
+}
+
+int dsg_comm_destroy(dsg_comm comm) {
+  return guarded([&] {
+    if (!comm) return;
+    nccl_comm_destroy(comm->nccl);
+    delete comm;
+  });
+}
+
+int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
+                        double cut_hi, dsg_model merged, int64_t* n_merged, double* ms) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    cudaEvent_t a, b;
+    DSG_CUDA_CHECK(cudaEventCreate(&a));
+    DSG_CUDA_CHECK(cudaEventCreate(&b));
+    DSG_CUDA_CHECK(cudaEventRecord(a, ctx->stream));
+    int64_t total = merge_allgather_dev(comm->nccl, comm->nranks, comm->rank, local->m, axis,
+                                        cut_lo, cut_hi, merged->m, ctx->frame.scan, ctx->stream);
+    DSG_CUDA_CHECK(cudaEventRecord(b, ctx->stream));
+    DSG_CUDA_CHECK(cudaEventSynchronize(b));
+    float t;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    merged->m.iteration = local->m.iteration;
+    merged->m.origin_partition = -1;
+    reset_optimizer(ctx, merged->m);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    if (n_merged) *n_merged = total;
+    if (ms) *ms = t;
+  });
+}
+
+int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const dsg_camera* cam_in,
+                           const dsg_render_config* cfg, double* rgb, double* ms) {
+  return guarded([&] {
+    RenderDev rd = make_rd(cfg);
+    CamDev cam = make_cam(cam_in);
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int R = comm ? comm->nranks : 1, me = comm ? comm->rank : 0;
+    // equal bands of tile rows
+    std::vector<int> t0(R), t1(R), r0(R), r1(R);
+    for (int r = 0; r < R; ++r) {
+      t0[r] = (int)((int64_t)cam.tiles_y * r / R);
+      t1[r] = (int)((int64_t)cam.tiles_y * (r + 1) / R);
+      r0[r] = std::min(t0[r] * kTile, cam.height);
+      r1[r] = std::min(t1[r] * kTile, cam.height);
+    }
+    CamDev band = cam;
+    band.band_ty0 = t0[me];
+    band.band_ty1 = t1[me];
+    cudaEvent_t a, b;
+    DSG_CUDA_CHECK(cudaEventCreate(&a));
+    DSG_CUDA_CHECK(cudaEventCreate(&b));
+    DSG_CUDA_CHECK(cudaEventRecord(a, st));
+    forward(ctx, model->m, band, rd);
+    if (R > 1) gather_bands_dev(comm->nccl, R, me, ctx->frame.rgb.get(), cam.width, cam.height, r0, r1, st);
+    DSG_CUDA_CHECK(cudaEventRecord(b, st));
+    DSG_CUDA_CHECK(cudaEventSynchronize(b));
+    float t;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&t, a, b));
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (ms) *ms = t;
+    if (rgb && me == 0) {
+      const int64_t npix = (int64_t)cam.width * cam.height;
+      double* d = ctx->stage_d.ensure(4 * npix);
+      k_render_out<<<nblk(npix), 256, 0, st>>>(ctx->frame.rgb.get(), ctx->frame.T.get(), npix, d,
+                                                d + 3 * npix);
+      count_launch();
+      DSG_CUDA_CHECK(cudaMemcpyAsync(rgb, d, sizeof(double) * 3 * npix, cudaMemcpyDeviceToHost, st));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+  });
 }
 
 int dsg_last_timing(dsg_ctx ctx, double* total_ms, double* stage_ms) {

@@ -39,7 +39,9 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
       int y0 = max(to_int_x86(ceil(ds(ds(pr.my, ry), 0.5))), 0);
       int y1 = min(to_int_x86(floor(ds(da(pr.my, ry), 0.5))), a.cam.height - 1);
       double det = ds(dm(pr.cxx, pr.cyy), dm(pr.cxy, pr.cxy));
-      if (x0 <= x1 && y0 <= y1 && det > 0.0) {
+      // tile-parallel global render: only splats reaching this rank's band
+      const int bty0 = max(y0 / kTile, a.cam.band_ty0), bty1 = min(y1 / kTile, a.cam.band_ty1 - 1);
+      if (x0 <= x1 && y0 <= y1 && det > 0.0 && bty0 <= bty1) {
         double ixx = dd(pr.cyy, det), ixy = dd(-pr.cxy, det), iyy = dd(pr.cxx, det);
         double op = sigmoid64(p[10]);
         // conditioning of the conic: bounds the fp32 rounding of q (guard band)
@@ -52,9 +54,9 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
         r[0] = make_float4(mxh, myh, (float)(pr.mx - (double)mxh), (float)(pr.my - (double)myh));
         r[1] = make_float4((float)ixx, (float)ixy, (float)iyy, (float)op);
         r[2] = make_float4((float)p[11], (float)p[12], (float)p[13], (float)kappa);
-        int tx0 = x0 / kTile, tx1 = x1 / kTile, ty0 = y0 / kTile, ty1 = y1 / kTile;
+        int tx0 = x0 / kTile, tx1 = x1 / kTile;
         a.trect[i] = make_int4(x0, y0, x1, y1);  // pixel rect; tile rect = rect / kTile
-        count = (uint32_t)((tx1 - tx0 + 1) * (ty1 - ty0 + 1));
+        count = (uint32_t)((tx1 - tx0 + 1) * (bty1 - bty0 + 1));
         a.depth[i] = pr.depth;
         double2* ex = a.exact + 3 * i;
         ex[0] = make_double2(pr.mx, pr.my);
@@ -115,7 +117,8 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv
 // depth order; tile enumeration row-major inside the rect (render.hpp:127-133).
 __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
                             const uint32_t* __restrict__ offs, const int4* __restrict__ trect,
-                            int tiles_x, uint32_t* __restrict__ tile_key,
+                            int tiles_x, int band_ty0, int band_ty1,
+                            uint32_t* __restrict__ tile_key,
                             uint32_t* __restrict__ dup_val, uint32_t* __restrict__ dup_base) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nv) return;
@@ -123,7 +126,8 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
   uint32_t o = offs[s];
   dup_base[i] = o;
   const int4 pr = trect[i];
-  const int4 r = make_int4(pr.x / kTile, pr.y / kTile, pr.z / kTile, pr.w / kTile);
+  const int4 r = make_int4(pr.x / kTile, max(pr.y / kTile, band_ty0), pr.z / kTile,
+                           min(pr.w / kTile, band_ty1 - 1));
   for (int ty = r.y; ty <= r.w; ++ty)
     for (int tx = r.x; tx <= r.z; ++tx) {
       tile_key[o] = (uint32_t)(ty * tiles_x + tx);
@@ -239,7 +243,8 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.tile_key2.ensure(std::max<uint32_t>(nd, 1));
   f.dup_val2.ensure(std::max<uint32_t>(nd, 1));
   k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(), cam.tiles_x,
-                                               f.tile_key.get(), f.dup_val.get(), f.dup_base.get());
+                                               cam.band_ty0, cam.band_ty1, f.tile_key.get(),
+                                               f.dup_val.get(), f.dup_base.get());
                                                count_launch();
   tm.mark(3, st);
   int tile_bits = 1;

@@ -25,6 +25,7 @@ struct CamDev {
   double near_plane;
   int width, height;
   int tiles_x, tiles_y;
+  int band_ty0, band_ty1;  // tile rows binned/blended: [band_ty0, band_ty1) (full image by default)
 };
 
 // Render-config constants as the kernels use them.

@@ -132,6 +132,29 @@ void knn_mean_dev(const double* host_pts, const double* pts, int64_t n, int k, d
 void seed_params_dev(const double* pts, const double* colors, const double* scale, int64_t n,
                      double fixed_ls, double opacity_logit, float* params, int64_t pitch,
                      cudaStream_t st);
+// partition_cloud (partition.hpp:42-104) on the device; lists in index order.
+struct PartitionResult {
+  int axis = 0;
+  std::vector<double> cut_lo, cut_hi, box;  // box: [k][lo xyz, hi xyz]
+  std::vector<std::vector<uint32_t>> owned, ghost;
+};
+PartitionResult partition_dev(const double* host_pts, int64_t n, int nparts, double margin,
+                              SortScratch& ss, ScanScratch& sc, cudaStream_t st);
+// merge_models keep rule (partition.hpp:120): compact splats whose mu[axis]
+// lies in [cut_lo, cut_hi) into dst (planar, pitch dpitch) at dst_off; returns
+// the survivor count (dst may be null to count only).
+int64_t merge_compact_dev(const float* src, int64_t spitch, int64_t n, int axis, double cut_lo,
+                          double cut_hi, float* dst, int64_t dpitch, int64_t dst_off,
+                          ScanScratch& sc, cudaStream_t st);
+// NCCL exchange (comm.cu): ghost-trim merge all-gather, band gather.
+void nccl_unique_id(uint8_t out[128]);
+void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
+void nccl_comm_destroy(void* comm);
+int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& local, int axis,
+                            double cut_lo, double cut_hi, ModelDev& merged, ScanScratch& sc,
+                            cudaStream_t st);
+void gather_bands_dev(void* comm, int nranks, int rank, float* rgb, int width, int height,
+                      const std::vector<int>& row0, const std::vector<int>& row1, cudaStream_t st);
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
                      double lambda, cudaStream_t st);
 

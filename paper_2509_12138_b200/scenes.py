@@ -61,16 +61,20 @@ def _jitter(rng, shape, amp):
     return (rng.random(shape) - 0.5) * amp
 
 
-def kingsnake(n: int = SIZES["kingsnake"], seed: int = 1, turns: float = 6.0, length: float = 1.0):
+def kingsnake(n: int = SIZES["kingsnake"], seed: int = 1, turns: float = 6.0):
     """Coiled tube: isosurface |p - helix(t)| = r(t), r banded like snake scales.
 
+    Coil radius, tube radius and pitch are fixed; `turns` sets the length
+    (6 turns = one unit), so a weak-scaled scene (N x points, N x turns) keeps
+    the point density and per-slab geometry of the single-GPU config.
     Points are spread area-uniformly: a (t, phi) lattice whose spacing is
     matched along and around the tube, with sub-cell jitter.
     """
     rng = np.random.default_rng(seed)
-    R = 0.22 * length           # coil radius
+    length = turns / 6.0
+    R = 0.22                    # coil radius
     pitch = length / turns      # rise per turn
-    r0 = 0.045 * length         # tube radius
+    r0 = 0.045                  # tube radius
     circ = 2 * math.pi * r0
     arc_per_turn = math.sqrt((2 * math.pi * R) ** 2 + pitch ** 2)
     L = arc_per_turn * turns

@@ -1,0 +1,118 @@
+"""GPU parity beyond the single-view path: seeding, view synthesis, device
+partitioning and merge, the tile-parallel render, and a config-1-scale
+train step (99,726-point sphere isosurface, 256^2 views).
+"""
+import numpy as np
+import pytest
+
+from oracle import Oracle
+from paper_2509_12138_b200 import api, scenes
+from paper_2509_12138_b200.types import RenderConfig, SplatModel, TrainConfig, TrainView
+from test_gpu_parity import assert_grads_close
+from util import fp32_exact, random_cloud, random_scene
+from util import test_camera as make_camera
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def orc():
+    return Oracle()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return api.Context(0)
+
+
+def test_knn_and_median_bit_exact(orc, ctx):
+    pts = random_cloud(3, 1500)
+    for k in (1, 3, 5):
+        np.testing.assert_array_equal(api.knn_mean_distances(pts, k, ctx=ctx),
+                                      orc.knn_mean_distances(pts, k))
+    assert api.median_nn_spacing(pts, ctx=ctx) == orc.median_nn_spacing(pts)
+    surf, _, _ = scenes.sphere(4000)
+    np.testing.assert_array_equal(api.knn_mean_distances(surf, 3, ctx=ctx),
+                                  orc.knn_mean_distances(surf, 3))
+
+
+def test_seed_and_gt_models(orc, ctx):
+    pts, cols, _ = scenes.sphere(3000)
+    a = api.seed_gaussians(pts, cols, 3, ctx=ctx).download().params
+    b = orc.seed_gaussians(pts, cols).params.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(a, b, rtol=2e-7, atol=0)
+    g = api.ground_truth_model(pts, cols, 0.01, 0.97, ctx=ctx).download().params
+    h = orc.ground_truth_model(pts, cols, 0.01).params.astype(np.float32).astype(np.float64)
+    np.testing.assert_allclose(g, h, rtol=2e-7, atol=0)
+
+
+def test_view_synthesis_matches_make_train_view(orc, ctx):
+    pts, cols, _ = scenes.sphere(6000)
+    nn = orc.median_nn_spacing(pts)
+    gt = orc.ground_truth_model(pts, cols, nn)
+    gt = fp32_exact(gt)
+    cams = scenes.rig_for_cloud(pts, 4, 2, 96)[:3]
+    dgt = api.DeviceModel(ctx, gt)
+    views = api.DeviceViews.synthesize(ctx, dgt, RenderConfig(), cams, pts, True, 2.0, 2.0)
+    for i, cam in enumerate(cams):
+        v = views.download(i)
+        ref = orc.render(gt, cam, RenderConfig()).color
+        assert np.max(np.abs(v.ground_truth - ref)) <= 1e-3
+        np.testing.assert_array_equal(v.mask, orc.render_mask(pts, cam, 2.0, 2.0))
+
+
+@pytest.mark.parametrize("nparts,margin", [(1, 0.25), (3, 0.15), (8, 0.3)])
+def test_device_partition_bit_exact(orc, ctx, nparts, margin):
+    pts = random_cloud(nparts + 9, 5000)
+    pts[::13, 0] = pts[0, 0]
+    pts[5, 0] = -0.0
+    pts[6, 0] = 0.0
+    a = api.partition_cloud(pts, nparts, margin, ctx=ctx)
+    b = orc.partition_cloud(pts, nparts, margin)
+    for pa, pb in zip(a, b):
+        assert pa.cut_axis == pb.cut_axis and pa.cut_lo == pb.cut_lo and pa.cut_hi == pb.cut_hi
+        np.testing.assert_array_equal(pa.owned_box, pb.owned_box)
+        np.testing.assert_array_equal(pa.owned_indices, pb.owned_indices)
+        np.testing.assert_array_equal(pa.ghost_indices, pb.ghost_indices)
+
+
+def test_device_merge_matches_oracle(orc, ctx):
+    pts = random_cloud(41, 400)
+    parts = orc.partition_cloud(pts, 3, 0.2)
+    rng = np.random.default_rng(1)
+    models = [fp32_exact(SplatModel(rng.uniform(-1.2, 1.2, size=(50 + 7 * k, 14)), 4 + k, k))
+              for k in range(3)]
+    merged = api.merge_models(models, parts, ctx=ctx).download()
+    keep = orc.merge_keep([m.params for m in models], parts)
+    np.testing.assert_array_equal(merged.params, np.concatenate([m.params for m in models])[keep])
+    assert merged.iteration == 6
+
+
+def test_render_distributed_single_rank_equals_render(ctx):
+    model = fp32_exact(random_scene(99, 300))
+    model.params[:, 3:6] -= 1.5
+    cam = make_camera(96)
+    dm = api.DeviceModel(ctx, model)
+    img, ms = api.render_distributed(None, dm, cam, RenderConfig())
+    ref = api.render(dm, cam, RenderConfig(), ctx=ctx).color
+    np.testing.assert_array_equal(img, ref)
+    assert ms > 0
+
+
+def test_config1_scale_train_step(orc, ctx):
+    """Config 1 shape: 99,726-point sphere isosurface, GT at the median NN
+    spacing, 256^2 views, kNN seeds; two train steps vs the oracle."""
+    pts, cols, _ = scenes.sphere()
+    nn = orc.median_nn_spacing(pts[:20000])  # O(N^2) oracle on a subset; value only sets scales
+    gt = fp32_exact(orc.ground_truth_model(pts, cols, nn))
+    cams = scenes.rig_for_cloud(pts, 16, 4, 256)[:2]
+    seeds = fp32_exact(SplatModel(api.seed_gaussians(pts, cols, 3, ctx=ctx).download().params))
+    views = [TrainView(c, orc.render(gt, c, RenderConfig()).color, orc.render_mask(pts, c, 2.0, 2.0))
+             for c in cams]
+    cfg = TrainConfig(iterations=2, seed=1)
+    a = api.train_partition_full(seeds, views, cfg, ctx=ctx, loss_trace=True)
+    b = orc.train_partition_full(seeds, views, cfg, loss_trace=True)
+    np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=1e-5)
+    # per-scalar Adam steps: ~lr*sign(g) on the first step
+    assert_grads_close(a.model.params - seeds.params, b.model.params - seeds.params, rtol=1e-4,
+                       floor=1e-3)

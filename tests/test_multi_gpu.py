@@ -1,0 +1,80 @@
+"""Multi-GPU exchange over NCCL (needs >= 2 GPUs): the ghost-trim merge
+all-gather equals merge_models, and the tile-parallel render gathered to rank
+0 equals the single-GPU render of the merged model."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+WORKER = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "tests"))
+import torch, torch.distributed as dist
+from paper_2509_12138_b200 import api
+from paper_2509_12138_b200.types import RenderConfig, SplatModel
+from util import random_cloud, random_scene, fp32_exact
+from util import test_camera as make_camera
+rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+torch.cuda.set_device(rank)
+dist.init_process_group("gloo")
+ctx = api.Context(rank)
+uid = [api.Comm.unique_id() if rank == 0 else None]
+dist.broadcast_object_list(uid, src=0)
+comm = api.Comm(ctx, uid[0], world, rank)
+pts = random_cloud(5, 4000)
+parts = api.partition_cloud(pts, world, 0.1, ctx=ctx)
+rng = np.random.default_rng(10 + rank)
+model = random_scene(50 + rank, 400)
+model.params[:, 0:3] = pts[np.concatenate([parts[rank].owned_indices, parts[rank].ghost_indices])[:400]]
+model.params[:, 3:6] -= 2.0
+model = fp32_exact(SplatModel(model.params, 7, rank))
+dm = api.DeviceModel(ctx, model)
+merged, n, ms = api.merge_allgather(comm, dm, parts[rank])
+allp = [None] * world
+dist.all_gather_object(allp, model.params)
+cam = make_camera(128)
+img, rms = api.render_distributed(comm, merged, cam, RenderConfig())
+if rank == 0:
+    ref_models = [SplatModel(p, 7, k) for k, p in enumerate(allp)]
+    from paper_2509_12138_b200.partition import merge_models
+    ref = merge_models(ref_models, parts)
+    got = merged.download()
+    assert np.array_equal(got.params, ref.params), "merged model differs"
+    single = api.render(api.DeviceModel(ctx, ref), cam, RenderConfig(), ctx=ctx).color
+    assert np.array_equal(img, single), np.max(np.abs(img - single))
+    print("MULTI_GPU_OK", n, ms, rms)
+comm.close()
+dist.barrier()
+dist.destroy_process_group()
+"""
+
+
+def _ngpus():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def test_merge_allgather_and_band_render_2gpu(tmp_path):
+    if _ngpus() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, ROOT=ROOT)
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), str(script)], capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0 and "MULTI_GPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
