@@ -56,6 +56,17 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
         r[2] = make_float4((float)p[11], (float)p[12], (float)p[13], (float)kappa);
         int tx0 = x0 / kTile, tx1 = x1 / kTile;
         a.trect[i] = make_int4(x0, y0, x1, y1);  // pixel rect; tile rect = rect / kTile
+        // Effective rect for the blend's sub-tile masks: alpha >= cutoff needs
+        // o*exp(-q/2) >= c, i.e. q <= 2 ln(o/c), so only pixels with
+        // |d| <= sqrt(q_eff * cov) can composite (widened by one pixel).
+        const double q_eff = fmin(a.rd.sigma_sq, 2.0 * log(op / a.rd.alpha_cutoff));
+        if (q_eff < 0.0) {
+          a.erect[i] = make_int4(1, 1, 0, 0);  // never composites anywhere
+        } else {
+          const double ex = sqrt(q_eff * pr.cxx), ey = sqrt(q_eff * pr.cyy);
+          a.erect[i] = make_int4((int)ceil(pr.mx - ex - 0.5) - 1, (int)ceil(pr.my - ey - 0.5) - 1,
+                                 (int)floor(pr.mx + ex - 0.5) + 1, (int)floor(pr.my + ey - 0.5) + 1);
+        }
         count = (uint32_t)((tx1 - tx0 + 1) * (bty1 - bty0 + 1));
         a.depth[i] = pr.depth;
         double2* ex = a.exact + 3 * i;
@@ -146,9 +157,9 @@ __global__ void k_entry_masks(const uint32_t* __restrict__ tile_key,
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nd) return;
   const uint32_t t = tile_key[e];
-  const int4 pr = prect[val[e]];
+  const int4 pr = prect[val[e]];  // effective rect, already widened by one pixel
   const int ox = (int)(t % (uint32_t)tiles_x) * kTile, oy = (int)(t / (uint32_t)tiles_x) * kTile;
-  const int x0 = pr.x - 1 - ox, x1 = pr.z + 1 - ox, y0 = pr.y - 1 - oy, y1 = pr.w + 1 - oy;
+  const int x0 = pr.x - ox, x1 = pr.z - ox, y0 = pr.y - oy, y1 = pr.w - oy;
   uint32_t m = 0;
 #pragma unroll
   for (int w = 0; w < 8; ++w) {
@@ -179,6 +190,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.tiles = (int64_t)cam.tiles_x * cam.tiles_y;
   f.rec.ensure(3 * (size_t)std::max<int64_t>(n, 1));
   f.trect.ensure(std::max<int64_t>(n, 1));
+  f.erect.ensure(std::max<int64_t>(n, 1));
   f.tcount.ensure(std::max<int64_t>(n, 1));
   f.depth.ensure(std::max<int64_t>(n, 1));
   f.exact.ensure(3 * (size_t)std::max<int64_t>(n, 1));
@@ -203,6 +215,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     a.rd = rd;
     a.rec = f.rec.get();
     a.trect = f.trect.get();
+    a.erect = f.erect.get();
     a.tcount = f.tcount.get();
     a.depth = f.depth.get();
     a.exact = f.exact.get();
@@ -256,7 +269,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get());
   count_launch();
   f.emask.ensure(std::max<uint32_t>(nd, 1));
-  k_entry_masks<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, f.sorted_val, f.trect.get(), nd,
+  k_entry_masks<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, f.sorted_val, f.erect.get(), nd,
                                                  cam.tiles_x, f.emask.get());
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());

@@ -11,6 +11,7 @@ struct PreprocessArgs {
   RenderDev rd;
   float4* rec;          // [n][3] blend payload (model order)
   int4* trect;          // [n] pixel rect (x0, y0, x1, y1), render.hpp:71-81
+  int4* erect;          // [n] effective (alpha >= cutoff) rect, widened by 1 px
   uint32_t* tcount;     // [n] overlapped tiles (0 = culled)
   double* depth;        // [n] camera-space depth (fp64)
   double2* exact;       // [n][3] fp64 (mx,my) (ixx,ixy) (iyy,op) for the guard band
@@ -26,7 +27,7 @@ struct Frame {
   int width = 0, height = 0;
   // per gaussian (model order)
   DevBuf<float4> rec;
-  DevBuf<int4> trect;
+  DevBuf<int4> trect, erect;
   DevBuf<uint32_t> tcount, dup_base;
   DevBuf<double> depth;
   DevBuf<double2> exact;     // [n][3] fp64 mean2d, conic, opacity

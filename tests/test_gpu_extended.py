@@ -112,7 +112,31 @@ def test_config1_scale_train_step(orc, ctx):
     cfg = TrainConfig(iterations=2, seed=1)
     a = api.train_partition_full(seeds, views, cfg, ctx=ctx, loss_trace=True)
     b = orc.train_partition_full(seeds, views, cfg, loss_trace=True)
-    np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=1e-5)
-    # per-scalar Adam steps: ~lr*sign(g) on the first step
-    assert_grads_close(a.model.params - seeds.params, b.model.params - seeds.params, rtol=1e-4,
-                       floor=1e-3)
+    # step 1 sees identical inputs; step 2 sees fp32 post-Adam params (<= 1e-4 relative)
+    np.testing.assert_allclose(a.loss_trace[:1], b.loss_trace[:1], rtol=1e-6)
+    np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=1e-4)
+
+    # One step: with epsilon = 1e-15 Adam moves every scalar by ~lr*sign(g)
+    # (adam.hpp:84-91), so post-Adam parity holds wherever the reference
+    # gradient is above the stated floor (1e-4 x the group's max |g|); below
+    # it the sign is fp noise and a flip moves the scalar by 2*lr.
+    cfg1 = TrainConfig(iterations=1, seed=1)
+    a1 = api.train_partition_full(seeds, views, cfg1, ctx=ctx)
+    b1 = orc.train_partition_full(seeds, views, cfg1)
+    order = api.view_order(1, len(views), 1)
+    v0 = views[int(order[0])]
+    ref = orc.render(seeds, v0.cam, RenderConfig())
+    g = orc.backward(seeds, v0.cam, RenderConfig(), ref,
+                     orc.masked_loss(ref.color, v0, cfg1.loss_lambda).dL_dpixels).grads
+    step_a, step_b = a1.model.params - seeds.params, b1.model.params - seeds.params
+    flips = 0
+    for name, sl in (("mu", slice(0, 3)), ("log_scale", slice(3, 6)), ("rot", slice(6, 10)),
+                     ("opacity", slice(10, 11)), ("color", slice(11, 14))):
+        gs = np.abs(g[:, sl])
+        strong = gs >= 1e-4 * gs.max() if gs.max() > 0 else np.zeros_like(gs, bool)
+        da, db = step_a[:, sl], step_b[:, sl]
+        tol = 1e-4 * np.abs(db) + 1e-6 * np.abs(db).max()
+        bad = np.abs(da - db) > tol
+        assert not (bad & strong).any(), (name, int((bad & strong).sum()))
+        flips += int(bad.sum())
+    assert flips <= 0.005 * step_a.size, flips
