@@ -170,7 +170,42 @@ def build_partition_inputs(args, dist: Dist, ctx):
         f"({len(part.owned_indices):,} owned + {len(part.ghost_indices):,} ghosts), nn {nn:.6g}, "
         f"{len(cams)} train views at {args.res}^2, setup {time.time() - t0:.1f}s")
     return dict(points=ppts, colors=pcols, cams=cams, views=views, seeds=seeds, gt=gt_model,
-                rcfg=rcfg, nn=nn, n_part=len(ppts), rig=rig, test_idx=test_idx)
+                rcfg=rcfg, nn=nn, n_part=len(ppts), rig=rig, test_idx=test_idx,
+                partition=part, center=(pts.min(0) + pts.max(0)) * 0.5)
+
+
+def global_phase(args, dist: Dist, ctx, inp, trained, reps: int = 3):
+    """Ghost-trim merge of the trained partitions (NCCL all-gather at N>1) and
+    the tile-parallel 3840x2160 render of the merged model (BASELINE configs[4]
+    shape; explicit camera since the rig builder is square-only)."""
+    from paper_2509_12138_b200.types import Camera
+    comm = None
+    if dist.world > 1:
+        import torch.distributed as tdist
+        uid = [api.Comm.unique_id() if dist.rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        comm = api.Comm(ctx, uid[0], dist.world, dist.rank)
+        merged, n_merged, merge_ms = api.merge_allgather(comm, trained, inp["partition"])
+    else:
+        t0 = time.perf_counter()
+        merged = api.merge_models([trained], [inp["partition"]], ctx=ctx)
+        merge_ms = (time.perf_counter() - t0) * 1e3
+        n_merged = merged.info()[0]
+    c0 = inp["rig"][0]
+    cam = Camera(c0.position, tuple(float(v) for v in inp["center"]), (0.0, 1.0, 0.0), 0.9, 3840,
+                 2160, c0.near, c0.far)
+    api.render_distributed(comm, merged, cam, inp["rcfg"], want_image=False)  # warm-up
+    ms = 0.0
+    for _ in range(reps):
+        dist.barrier()
+        _, t = api.render_distributed(comm, merged, cam, inp["rcfg"], want_image=False)
+        ms += dist.max(t)
+    if comm:
+        comm.close()
+    mpix = reps * 3840 * 2160 / (ms * 1e-3) / 1e6
+    return {"merged_gaussians": int(n_merged), "merge_allgather_ms": round(dist.max(merge_ms), 3),
+            "render_4k_ms": round(ms / reps, 3), "render_4k_mpix_per_sec": round(mpix, 1),
+            "render_ranks": dist.world}
 
 
 def split_rig(n_views: int, test_fraction: float, seed: int):
@@ -284,6 +319,9 @@ def run_ours(args, dist: Dist):
     total_iters = args.steps * dist.world
     gv = dist.sum(float(n) * args.steps) / t_max
 
+    # merge of the trained partitions + tile-parallel 4K render (untimed w.r.t. value)
+    glob = global_phase(args, dist, ctx, inp, dm) if not args.no_global else None
+
     # per-stage profile (separate run; events + sync per step)
     ctx.set_profiling(True)
     dm.upload(seeds_host)
@@ -360,6 +398,7 @@ def run_ours(args, dist: Dist):
         "roofline": roof,
         "cpu_baseline": cpu,
         "clocks": clk,
+        "global": glob,
         "final_loss": fl,
     }
     return line
@@ -442,6 +481,7 @@ def main():
     ap.add_argument("--az", type=int, default=28)
     ap.add_argument("--el", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-global", action="store_true", help="skip the merge + 4K render phase")
     args = ap.parse_args()
     if args.n_per_gpu is None:
         args.n_per_gpu = scenes.SIZES[args.workload]
