@@ -485,6 +485,10 @@ def main():
     args = ap.parse_args()
     if args.n_per_gpu is None:
         args.n_per_gpu = scenes.SIZES[args.workload]
+    # Libraries (NCCL's version banner, torchrun) may write to fd 1: keep the
+    # real stdout for the single JSON line and send everything else to stderr.
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     dist = Dist()
     if args.gpus != dist.world:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {dist.world}; using WORLD_SIZE")
@@ -493,7 +497,8 @@ def main():
     else:
         line = run_ours(args, dist)
     if dist.rank == 0 and line is not None:
-        print(json.dumps(line), flush=True)
+        json_out.write(json.dumps(line) + "\n")
+        json_out.flush()
     dist.close()
 
 

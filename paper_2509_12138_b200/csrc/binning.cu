@@ -177,6 +177,38 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd,
   if (e == nd - 1 || tile_key[e + 1] != t) ranges[t].y = (uint32_t)(e + 1);
 }
 
+// Longest-first tile schedule for the blend kernels: tiles are bucketed by
+// floor(log2(list length)) and emitted heaviest bucket first, so the long
+// lists start early instead of forming the tail (order inside a bucket is
+// irrelevant: tiles are independent).
+__global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t* bins,
+                            uint32_t* counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const uint2 r = ranges[t0 + i];
+  const uint32_t len = r.y - r.x;
+  const uint32_t b = len ? 32u - __clz(len) : 0u;  // 0..32
+  bins[i] = b;
+  atomicAdd(&counts[b], 1u);
+}
+
+__global__ void k_tile_bin_offsets(uint32_t* counts) {  // one warp: descending exclusive scan
+  const int lane = threadIdx.x;
+  uint32_t run = 0;
+  for (int b = 32; b >= 0; --b) {
+    const uint32_t c = counts[b];
+    if (lane == 0) counts[b] = run;
+    run += c;
+  }
+}
+
+__global__ void k_tile_order(const uint32_t* __restrict__ bins, int t0, int nt, uint32_t* counts,
+                             uint32_t* order) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  order[atomicAdd(&counts[bins[i]], 1u)] = (uint32_t)(t0 + i);
+}
+
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
@@ -272,6 +304,19 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   k_entry_masks<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, f.sorted_val, f.erect.get(), nd,
                                                  cam.tiles_x, f.emask.get());
   count_launch();
+  {
+    const int t0 = cam.band_ty0 * cam.tiles_x;
+    const int nt = (cam.band_ty1 - cam.band_ty0) * cam.tiles_x;
+    f.tile_order.ensure(std::max(nt, 1));
+    f.tile_bins.ensure(std::max(nt, 1) + 33);
+    uint32_t* counts = f.tile_bins.get() + std::max(nt, 1);
+    DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, 33 * sizeof(uint32_t), st));
+    k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, f.tile_bins.get(), counts);
+    k_tile_bin_offsets<<<1, 32, 0, st>>>(counts);
+    k_tile_order<<<blocks(nt, 256), 256, 0, st>>>(f.tile_bins.get(), t0, nt, counts,
+                                                  f.tile_order.get());
+    count_launch(3);
+  }
   DSG_CUDA_CHECK(cudaGetLastError());
   tm.mark(4, st);
 }

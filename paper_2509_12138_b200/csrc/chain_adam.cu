@@ -18,6 +18,7 @@ namespace dsg {
 
 namespace {
 
+#if 0  // K7 moved to chain.cu (precision-templated); kept here for reference until removed
 // d R(q)/d q_k for a unit quaternion (backward.hpp:43-69).
 __device__ __forceinline__ void drot(const double* q, int k, double* m) {
   const double w = q[0], x = q[1], y = q[2], z = q[3];
@@ -222,6 +223,7 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
   a.dmean[P + i] = (float)gmy;
   a.touch[i] = 1;
 }
+#endif
 
 __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -260,13 +262,6 @@ __global__ void __launch_bounds__(256) k_adam(AdamArgs a) {
 }
 
 }  // namespace
-
-void chain_3d(const ChainArgs& a, cudaStream_t st) {
-  if (a.n == 0) return;
-  k_chain<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a);
-  count_launch();
-  DSG_CUDA_CHECK(cudaGetLastError());
-}
 
 void adam_update(const AdamArgs& a, cudaStream_t st) {
   if (a.n == 0) return;

