@@ -203,7 +203,10 @@ def global_phase(args, dist: Dist, ctx, inp, trained, reps: int = 3):
     if comm:
         comm.close()
     mpix = reps * 3840 * 2160 / (ms * 1e-3) / 1e6
-    return {"merged_gaussians": int(n_merged), "merge_allgather_ms": round(dist.max(merge_ms), 3),
+    mm = dist.max(merge_ms)
+    wire = 56.0 * int(n_merged) * (dist.world - 1) / max(dist.world, 1)  # bytes into each GPU
+    return {"merged_gaussians": int(n_merged), "merge_allgather_ms": round(mm, 3),
+            "merge_allgather_GBps_per_gpu": round(wire / (mm * 1e-3) / 1e9, 1) if dist.world > 1 else None,
             "render_4k_ms": round(ms / reps, 3), "render_4k_mpix_per_sec": round(mpix, 1),
             "render_ranks": dist.world}
 

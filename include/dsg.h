@@ -211,7 +211,8 @@ int dsg_comm_create(dsg_ctx ctx, const uint8_t* id128, int32_t nranks, int32_t r
 int dsg_comm_destroy(dsg_comm comm);
 /* Distributed merge: trim this rank's partition model to its owned slab,
  * all-gather survivor counts, broadcast survivors so every rank holds the
- * merged model in (partition = rank, index) order. *ms = device time. */
+ * merged model in (partition = rank, index) order. *ms = device time of
+ * the survivor exchange (the NCCL broadcast group, 56 B per survivor). */
 int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
                         double cut_hi, dsg_model merged, int64_t* n_merged, double* ms);
 /* Tile-parallel render (comm may be NULL): rank r bins and blends tile-row

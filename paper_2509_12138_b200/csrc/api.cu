@@ -1175,12 +1175,12 @@ int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axi
     DSG_CUDA_CHECK(cudaEventCreate(&a));
     DSG_CUDA_CHECK(cudaEventCreate(&b));
     DSG_CUDA_CHECK(cudaEventRecord(a, ctx->stream));
+    float t = 0.f;  // device time of the survivor exchange (NCCL group)
     int64_t total = merge_allgather_dev(comm->nccl, comm->nranks, comm->rank, local->m, axis,
-                                        cut_lo, cut_hi, merged->m, ctx->frame.scan, ctx->stream);
+                                        cut_lo, cut_hi, merged->m, ctx->frame.scan, ctx->stream,
+                                        &t);
     DSG_CUDA_CHECK(cudaEventRecord(b, ctx->stream));
     DSG_CUDA_CHECK(cudaEventSynchronize(b));
-    float t;
-    DSG_CUDA_CHECK(cudaEventElapsedTime(&t, a, b));
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     merged->m.iteration = local->m.iteration;

@@ -111,7 +111,7 @@ void nccl_comm_destroy(void* c) {
 // Steps 1-3 above. `merged` receives the merged model (reserved inside).
 int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& local, int axis,
                             double cut_lo, double cut_hi, ModelDev& merged, ScanScratch& sc,
-                            cudaStream_t st) {
+                            cudaStream_t st, float* wire_ms) {
   Nccl& N = nccl();
   ncclComm_t c = (ncclComm_t)comm;
   // 1. local compaction into a dense [14][cnt] buffer
@@ -138,6 +138,10 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& lo
   // 3. every rank's survivors, broadcast row by row into the merged model
   merged.reserve(std::max<int64_t>(total, 1));
   merged.n = total;
+  cudaEvent_t e0, e1;
+  DSG_CUDA_CHECK(cudaEventCreate(&e0));
+  DSG_CUDA_CHECK(cudaEventCreate(&e1));
+  DSG_CUDA_CHECK(cudaEventRecord(e0, st));
   nc(N.GroupStart(), "group start");
   for (int r = 0; r < nranks; ++r) {
     if (hc[r] == 0) continue;
@@ -149,7 +153,13 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& lo
     }
   }
   nc(N.GroupEnd(), "group end");
+  DSG_CUDA_CHECK(cudaEventRecord(e1, st));
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  float t = 0.f;
+  DSG_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (wire_ms) *wire_ms = t;
   return total;
 }
 

@@ -154,7 +154,7 @@ void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(void* comm);
 int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& local, int axis,
                             double cut_lo, double cut_hi, ModelDev& merged, ScanScratch& sc,
-                            cudaStream_t st);
+                            cudaStream_t st, float* wire_ms = nullptr);
 void gather_bands_dev(void* comm, int nranks, int rank, float* rgb, int width, int height,
                       const std::vector<int>& row0, const std::vector<int>& row1, cudaStream_t st);
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
