@@ -182,9 +182,9 @@ int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t v, double* ground_t
 
 /* train_partition_full (trainer.hpp:140-211): the whole loop on the device.
  * The model is updated in place (iteration advances). progress may be NULL;
- * loss_trace (capacity iterations) may be NULL. Densification events are
- * not yet supported on the device and return InvalidArgument before any
- * step runs. */
+ * loss_trace (capacity iterations) may be NULL. Densification and pruning
+ * (trainer.hpp:47-107, 195-202) run on the device; the model may change
+ * size (dsg_model_info reports the new count). */
 int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_config* cfg,
               int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
               double* loss_trace);

@@ -69,6 +69,7 @@ struct dsg_ctx_s {
   DevBuf<double> loss_trace;
   StageTimer timer;
   bool timer_init = false;
+  ModelDev spare;  // densification output storage (swapped with the model's)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   double* host_loss = nullptr;  // pinned, end-to-end mode
   double last_total_ms = 0.0;
@@ -760,10 +761,10 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     if (cfg->iterations == 0) return;
     const int64_t iters = cfg->iterations;
     const int64_t until = (int64_t)(cfg->densify_stop_fraction * (double)iters);
-    if (cfg->densify_interval > 0)
-      for (int64_t it = 0; it < iters; ++it)
-        if ((it + 1) % cfg->densify_interval == 0 && (it + 1) < until)
-          fail(kInvalidArgument, "densification is not yet implemented on the device");
+    // Rng densify_rng(seed ^ 0xd3a51f11) (trainer.hpp:165): splitmix64 state
+    // after the constructor's two warm-up draws (rng.hpp:25-30)
+    uint64_t drng = (cfg->seed ^ 0xd3a51f11ULL) ^ 0x853c49e6748fea9bULL;
+    drng += 2 * 0x9e3779b97f4a7c15ULL;
     RenderDev rd = make_rd(&cfg->render);
     std::vector<CamDev> cams;
     for (const auto& c : views->cams) cams.push_back(make_cam(&c));
@@ -853,6 +854,10 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
       m.adam_step += 1;
       adam_update(make_adam(m, rates, cfg->adam, m.adam_step, true), st);
       m.iteration += 1;
+      // densify at (it+1) % interval == 0 while (it+1) < stop (trainer.hpp:195-202)
+      if (cfg->densify_interval > 0 && (it + 1) % cfg->densify_interval == 0 && (it + 1) < until)
+        densify_dev(m, ctx->spare, cfg->prune_opacity, cfg->densify_grad_threshold,
+                    cfg->split_scale_threshold, drng, ctx->frame.scan, st);
       tm.mark(9, st);
       if (tm.on) {
         DSG_CUDA_CHECK(cudaEventSynchronize(tm.ev[9]));

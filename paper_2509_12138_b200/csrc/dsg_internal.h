@@ -50,6 +50,10 @@ struct DevBuf {
     return ptr;
   }
   T* get() const { return ptr; }
+  void swap(DevBuf& o) {
+    std::swap(ptr, o.ptr);
+    std::swap(cap, o.cap);
+  }
 };
 
 // Scratch for the radix sort and scans.

@@ -148,6 +148,16 @@ PartitionResult partition_dev(const double* host_pts, int64_t n, int nparts, dou
 int64_t merge_compact_dev(const float* src, int64_t spitch, int64_t n, int axis, double cut_lo,
                           double cut_hi, float* dst, int64_t dpitch, int64_t dst_off,
                           ScanScratch& sc, cudaStream_t st);
+// densify_and_prune + AdamState::remap on the device (densify.cu). `spare`
+// provides the output storage and receives the old one; rng_state is the
+// persistent splitmix64 state of the run's densify Rng (advanced in place).
+struct DensifyResult {
+  int64_t before = 0, after = 0, splits = 0;
+};
+DensifyResult densify_dev(ModelDev& m, ModelDev& spare, double prune_opacity, double grad_thr,
+                          double split_thr_cfg, uint64_t& rng_state, ScanScratch& sc,
+                          cudaStream_t st);
+
 // NCCL exchange (comm.cu): ghost-trim merge all-gather, band gather.
 void nccl_unique_id(uint8_t out[128]);
 void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);

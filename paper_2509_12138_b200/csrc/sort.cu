@@ -23,7 +23,10 @@ constexpr int kRadixBits = 8;
 constexpr int kRadix = 256;
 constexpr int kSortThreads = 256;
 constexpr int kSortWarps = kSortThreads / 32;
-constexpr int kSortItems = 12;
+#ifndef DSG_SORT_ITEMS
+#define DSG_SORT_ITEMS 16
+#endif
+constexpr int kSortItems = DSG_SORT_ITEMS;
 constexpr int kPart = kSortThreads * kSortItems;  // keys per partition
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
@@ -39,25 +42,45 @@ template <class K>
 __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, int64_t n,
                                                     int begin_bit, int passes,
                                                     uint32_t* __restrict__ ghist) {
-  __shared__ uint32_t h[8][kRadix];
-  for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&h[0][0])[i] = 0;
+  // 4 copies (one per warp pair) of up to 8 passes x 256 bins. Each thread
+  // counts runs of equal digits in registers and flushes a run with one
+  // shared atomic: high digits of sort keys are nearly constant, so this
+  // removes the same-address contention that serialises per-key atomics.
+  constexpr int kCopies = 4;
+  __shared__ uint32_t h[kCopies][8][kRadix];
+  for (int i = threadIdx.x; i < kCopies * 8 * kRadix; i += blockDim.x) (&h[0][0][0])[i] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = base + threadIdx.x;
-    bool valid = i < n;
-    K k = valid ? keys[i] : K(0);
-    for (int p = 0; p < passes; ++p) {
-      uint32_t d = valid ? (uint32_t)((k >> (begin_bit + kRadixBits * p)) & (kRadix - 1)) : 0x100u;
-      // warp-aggregated increment: keys are often clustered in one digit
-      uint32_t peers = __match_any_sync(0xffffffffu, d);
-      if (valid && (__ffs(peers) - 1) == lane) atomicAdd(&h[p][d], __popc(peers));
+  const int cp = (threadIdx.x >> 5) & (kCopies - 1);
+  uint32_t cur[8], cnt[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p) {
+    cur[p] = 0;
+    cnt[p] = 0;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const K k = keys[i];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      if (p >= passes) break;
+      const uint32_t d = (uint32_t)((k >> (begin_bit + kRadixBits * p)) & (kRadix - 1));
+      if (d != cur[p] && cnt[p]) {
+        atomicAdd(&h[cp][p][cur[p]], cnt[p]);
+        cnt[p] = 0;
+      }
+      cur[p] = d;
+      ++cnt[p];
     }
   }
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+    if (p < passes && cnt[p]) atomicAdd(&h[cp][p][cur[p]], cnt[p]);
   __syncthreads();
   for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
-    uint32_t v = (&h[0][0])[i];
+    const int p = i / kRadix, d = i % kRadix;
+    uint32_t v = 0;
+#pragma unroll
+    for (int c = 0; c < kCopies; ++c) v += h[c][p][d];
     if (v) atomicAdd(&ghist[i], v);
   }
 }
@@ -139,13 +162,28 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   } else {
     vs[(size_t)part * kRadix + d] = kFlagAgg | total;
     int64_t p = (int64_t)part - 1;
+    // read 4 predecessors per round trip (partition 0 always holds a prefix)
     while (true) {
-      uint32_t s = vs[(size_t)p * kRadix + d];
-      uint32_t flag = s & ~kValueMask;
-      if (flag == 0) continue;
-      excl += s & kValueMask;
-      if (flag == kFlagPrefix) break;
-      --p;
+      uint32_t s[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s[j] = 2u << 30;  // kFlagPrefix, total 0: before partition 0
+        if (p - j >= 0) s[j] = vs[(size_t)(p - j) * kRadix + d];
+      }
+      int j = 0;
+      bool done = false;
+#pragma unroll
+      for (; j < 4; ++j) {
+        const uint32_t flag = s[j] & ~kValueMask;
+        if (flag == 0) break;  // not published yet: resume from p - j
+        excl += s[j] & kValueMask;
+        if (flag == kFlagPrefix) {
+          done = true;
+          break;
+        }
+      }
+      if (done) break;
+      p -= j;
     }
     vs[(size_t)part * kRadix + d] = kFlagPrefix | (excl + total);
   }

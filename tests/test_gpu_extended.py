@@ -140,3 +140,23 @@ def test_config1_scale_train_step(orc, ctx):
         assert not (bad & strong).any(), (name, int((bad & strong).sum()))
         flips += int(bad.sum())
     assert flips <= 0.005 * step_a.size, flips
+
+
+@pytest.mark.parametrize("split_thr", [0.2, 0.0])
+def test_train_with_densify_matches_oracle(orc, ctx, split_thr):
+    """Clone / split / prune events on the device (trainer.hpp:47-107, 195-202):
+    same model size and per-splat parameters as the oracle, which is pinned
+    bit-exact to the reference (test_oracle_pin.test_train_densify_bit_exact)."""
+    cam = make_camera(32)
+    init = fp32_exact(random_scene(45, 8))
+    init.params[0, 3:6] = np.log(np.float32(0.5))
+    init.params[1, 10] = -9.0
+    gt = orc.render(fp32_exact(random_scene(46, 8)), cam, RenderConfig()).color
+    views = [TrainView(cam, gt, np.ones((32, 32)))]
+    cfg = TrainConfig(iterations=60, seed=4, densify_interval=10, densify_grad_threshold=1e-5,
+                      split_scale_threshold=split_thr)
+    a = api.train_partition_full(init, views, cfg, ctx=ctx, loss_trace=True)
+    b = orc.train_partition_full(init, views, cfg, loss_trace=True)
+    assert len(a.model) == len(b.model) and len(a.model) != len(init)
+    np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=2e-3)
+    np.testing.assert_allclose(a.model.params, b.model.params, rtol=0, atol=5e-3)
