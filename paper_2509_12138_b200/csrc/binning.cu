@@ -81,14 +81,40 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
   }
   // warp-aggregated compaction of the visible set (order fixed by the sort)
   uint32_t mask = __ballot_sync(0xffffffffu, vis);
-  if (mask == 0) return;
   uint32_t base = 0;
-  if (lane == __ffs(mask) - 1) base = atomicAdd(a.vis_count, (uint32_t)__popc(mask));
-  base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
+  if (mask != 0 && lane == __ffs(mask) - 1) base = atomicAdd(a.vis_count, (uint32_t)__popc(mask));
+  base = __shfl_sync(0xffffffffu, base, mask != 0 ? __ffs(mask) - 1 : 0);
   if (vis) {
     uint32_t slot = base + __popc(mask & ((1u << lane) - 1u));
     a.vis_key[slot] = __float_as_uint(depth_f);
     a.vis_idx[slot] = (uint32_t)i;
+  }
+  // key range of the visible set: the depth sort only needs the bits of
+  // (key - min), typically 24 of 32 (3 radix passes instead of 4)
+  uint32_t kmin = vis ? __float_as_uint(depth_f) : 0xffffffffu;
+  uint32_t kmax = vis ? __float_as_uint(depth_f) : 0u;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+  }
+  // one pair of atomics per block, and only when it can move the bound
+  // (same-address atomics from every warp serialise in L2)
+  __shared__ uint32_t smin[8], smax[8];
+  const int warp = threadIdx.x >> 5;
+  if (lane == 0) {
+    smin[warp] = kmin;
+    smax[warp] = kmax;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      kmin = min(kmin, smin[w]);
+      kmax = max(kmax, smax[w]);
+    }
+    volatile uint32_t* c = a.vis_count;
+    if (kmin < c[1]) atomicMin(a.vis_count + 1, kmin);
+    if (kmax > c[2]) atomicMax(a.vis_count + 2, kmax);
   }
 }
 
@@ -235,6 +261,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.ranges.ensure(f.tiles);
   f.counters.ensure(4);
   DSG_CUDA_CHECK(cudaMemsetAsync(f.counters.get(), 0, 4 * sizeof(uint32_t), st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(f.counters.get() + 1, 0xff, sizeof(uint32_t), st));  // key min
   DSG_CUDA_CHECK(cudaMemsetAsync(f.ranges.get(), 0, f.tiles * sizeof(uint2), st));
   f.n_visible = 0;
   f.n_dup = 0;
@@ -258,16 +285,21 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     count_launch();
     DSG_CUDA_CHECK(cudaGetLastError());
     tm.mark(1, st);
-    uint32_t nv = 0;
-    DSG_CUDA_CHECK(cudaMemcpyAsync(&nv, f.counters.get(), sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    uint32_t c3[3] = {0, 0, 0};
+    DSG_CUDA_CHECK(cudaMemcpyAsync(c3, f.counters.get(), 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-    f.n_visible = nv;
+    f.n_visible = c3[0];
+    f.key_min = c3[1];
+    f.key_max = c3[2];
   }
   const int64_t nv = f.n_visible;
   if (nv == 0) return;
+  int depth_bits = 1;
+  while (depth_bits < 32 && ((uint64_t)(f.key_max - f.key_min) >> depth_bits) != 0) ++depth_bits;
   // depth sort of the visible set (stable; key = fp32 depth bits)
   bool alt = radix_sort_pairs<uint32_t>(f.vis_key.get(), f.vis_idx.get(), f.vis_key2.get(),
-                                         f.vis_idx2.get(), nv, 0, 32, f.sort, st);
+                                         f.vis_idx2.get(), nv, 0, depth_bits, f.sort, st,
+                                         f.key_min);
   uint32_t* skey = alt ? f.vis_key2.get() : f.vis_key.get();
   uint32_t* sidx = alt ? f.vis_idx2.get() : f.vis_idx.get();
   k_depth_fixup<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get());

@@ -24,6 +24,7 @@ struct PreprocessArgs {
 // loss buffers and backward partials.
 struct Frame {
   int64_t n = 0, n_visible = 0, n_dup = 0, tiles = 0;
+  uint32_t key_min = 0, key_max = 0;  // fp32 depth-key range of the visible set
   int width = 0, height = 0;
   // per gaussian (model order)
   DevBuf<float4> rec;

@@ -27,6 +27,10 @@ constexpr int kSortWarps = kSortThreads / 32;
 #define DSG_SORT_ITEMS 16
 #endif
 constexpr int kSortItems = DSG_SORT_ITEMS;
+#ifndef DSG_LOOKBACK
+#define DSG_LOOKBACK 16
+#endif
+constexpr int kLookback = DSG_LOOKBACK;
 constexpr int kPart = kSortThreads * kSortItems;  // keys per partition
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
@@ -40,7 +44,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 template <class K>
 __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, int64_t n,
-                                                    int begin_bit, int passes,
+                                                    int begin_bit, int passes, K offset,
                                                     uint32_t* __restrict__ ghist) {
   // 4 copies (one per warp pair) of up to 8 passes x 256 bins. Each thread
   // counts runs of equal digits in registers and flushes a run with one
@@ -59,7 +63,7 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const K k = keys[i];
+    const K k = keys[i] - offset;
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       if (p >= passes) break;
@@ -108,8 +112,8 @@ struct OnesweepSmem {
 template <class K>
 __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
-    uint32_t* __restrict__ vout, int64_t n, int shift, const uint32_t* __restrict__ gscan,
-    uint32_t* status, uint32_t* counter) {
+    uint32_t* __restrict__ vout, int64_t n, int shift, K offset,
+    const uint32_t* __restrict__ gscan, uint32_t* status, uint32_t* counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem<K>& sm = *reinterpret_cast<OnesweepSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -130,7 +134,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     bool valid = idx < n;
     k[i] = valid ? kin[idx] : K(0);
     v[i] = valid ? vin[idx] : 0u;
-    dig[i] = valid ? (uint32_t)((k[i] >> shift) & (kRadix - 1)) : 0x100u;
+    dig[i] = valid ? (uint32_t)(((K)(k[i] - offset) >> shift) & (kRadix - 1)) : 0x100u;
   }
   const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -162,18 +166,20 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   } else {
     vs[(size_t)part * kRadix + d] = kFlagAgg | total;
     int64_t p = (int64_t)part - 1;
-    // read 4 predecessors per round trip (partition 0 always holds a prefix)
+    // read kLookback predecessors per round trip (partition 0 always holds a
+    // prefix): the first wave of resident partitions otherwise walks back
+    // through hundreds of aggregates one L2 round trip at a time
     while (true) {
-      uint32_t s[4];
+      uint32_t s[kLookback];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < kLookback; ++j) {
         s[j] = 2u << 30;  // kFlagPrefix, total 0: before partition 0
         if (p - j >= 0) s[j] = vs[(size_t)(p - j) * kRadix + d];
       }
       int j = 0;
       bool done = false;
 #pragma unroll
-      for (; j < 4; ++j) {
+      for (; j < kLookback; ++j) {
         const uint32_t flag = s[j] & ~kValueMask;
         if (flag == 0) break;  // not published yet: resume from p - j
         excl += s[j] & kValueMask;
@@ -207,7 +213,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   const int count = remain < kPart ? (int)remain : kPart;
   for (int j = tid; j < count; j += kSortThreads) {
     K key = sm.keys[j];
-    uint32_t dg = (uint32_t)((key >> shift) & (kRadix - 1));
+    uint32_t dg = (uint32_t)(((K)(key - offset) >> shift) & (kRadix - 1));
     uint32_t out = sm.global_base[dg] + (uint32_t)j - sm.block_excl[dg];
     kout[out] = key;
     vout[out] = sm.vals[j];
@@ -300,7 +306,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratc
 
 template <class K>
 bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
-                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st) {
+                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset) {
   if (n <= 1 || end_bit <= begin_bit) return false;
   if (n > (int64_t)kValueMask) fail(kInvalidArgument, "radix sort: too many keys");
   const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
@@ -312,7 +318,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
   DSG_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * passes * parts * kRadix, st));
   DSG_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * passes, st));
   int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, hist);
+  k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, offset, hist);
   count_launch();
   // Which digits actually vary? (a single populated bin = identity pass)
   s.host_hist.resize((size_t)passes * kRadix);
@@ -336,9 +342,9 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
     K* ko = in_alt ? keys : keys_alt;
     uint32_t* vo = in_alt ? vals : vals_alt;
     k_onesweep<K><<<(unsigned)parts, kSortThreads, smem, st>>>(
-        ki, vi, ko, vo, n, begin_bit + kRadixBits * p, hist + (size_t)p * kRadix,
+        ki, vi, ko, vo, n, begin_bit + kRadixBits * p, offset, hist + (size_t)p * kRadix,
         status + (size_t)p * parts * kRadix, counters + p);
-        count_launch();
+    count_launch();
     in_alt = !in_alt;
   }
   DSG_CUDA_CHECK(cudaGetLastError());
@@ -346,8 +352,8 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
 }
 
 template bool radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t, int,
-                                         int, SortScratch&, cudaStream_t);
+                                         int, SortScratch&, cudaStream_t, uint32_t);
 template bool radix_sort_pairs<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, int64_t, int,
-                                         int, SortScratch&, cudaStream_t);
+                                         int, SortScratch&, cudaStream_t, uint64_t);
 
 }  // namespace dsg
