@@ -193,7 +193,8 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
 /* partition_cloud (partition.hpp:42-104) on the device: positions [n][3];
  * cut_lo/cut_hi [nparts], owned_box [nparts][6] (lo xyz, hi xyz), per-part
  * counts, and owned/ghost index lists concatenated in partition order
- * (capacity cap each), every list in ascending point index. */
+ * (capacity cap each), every list in ascending point index. With
+ * owned_idx or ghost_idx NULL only the counts are written (size query). */
 int dsg_partition(dsg_ctx ctx, const double* positions, int64_t n, int32_t nparts, double margin,
                   int32_t* axis, double* cut_lo, double* cut_hi, double* owned_box,
                   int64_t* owned_count, int64_t* ghost_count, uint32_t* owned_idx,
@@ -232,6 +233,11 @@ int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32
 /* Page-lock caller memory for the end-to-end path (cudaHostRegister). */
 int dsg_host_register(void* ptr, int64_t bytes);
 int dsg_host_unregister(void* ptr);
+
+/* NVTX range around a region (lets `ncu --nvtx --nvtx-include name/`
+ * profile exactly the bench's timed steps). */
+int dsg_nvtx_push(const char* name);
+int dsg_nvtx_pop(void);
 
 /* Record per-stage CUDA events inside dsg_train (adds one sync per step). */
 int dsg_set_profiling(dsg_ctx ctx, int32_t enable);

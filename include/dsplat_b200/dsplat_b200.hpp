@@ -19,9 +19,11 @@
 //                     trainer.hpp:140 / :214        dsplat::b200::train_partition_full / ...
 //   seed_gaussians / median_nn_spacing / ground_truth_model
 //                     seed.hpp:49 / :39 / :78       dsplat::b200::...
-//   build_orbital_cameras, split_rig, partition_cloud, owns, merge_models:
-//     host-side, unchanged from the reference (camera.hpp:75-130,
-//     partition.hpp:34-126) — they are not on the device path.
+//   partition_cloud   partition.hpp:42              dsplat::b200::partition_cloud
+//   build_orbital_cameras, split_rig, owns: host-side, unchanged from the
+//     reference (camera.hpp:75-130, partition.hpp:34-40). merge_models of
+//     device-resident models is dsg_merge_models / dsg_merge_allgather in the
+//     C ABI (the trained models never leave the GPU).
 //
 // Errors: every failing call throws dsplat::Error with the same ErrorCode and
 // what() text ("<Code>: msg") the reference throws (error.hpp:57-61).
@@ -29,6 +31,7 @@
 // lazily creates one on device 0 for the calling thread.
 #pragma once
 
+#include <algorithm>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -38,6 +41,7 @@
 #include "dsg.h"
 #include "dsplat/error.hpp"
 #include "dsplat/loss.hpp"
+#include "dsplat/partition.hpp"
 #include "dsplat/render.hpp"
 #include "dsplat/seed.hpp"
 #include "dsplat/trainer.hpp"
@@ -334,11 +338,12 @@ inline TrainResult train_partition_full(const SplatModel& input,
   auto cb = [](int64_t it, double loss, void* u) { (*static_cast<Ctx*>(u)->p)(it, loss); };
   check(dsg_train(ctx.get(), dm.h, dv, &tc, shards, progress ? +cb : nullptr, &pc,
                   &result.final_loss, nullptr));
-  std::vector<double> p(14 * input.size());
-  int64_t n = 0, it = 0;
+  // densify/prune may have resized the model on the device
+  int64_t n = 0, it = 0, adam_steps = 0;
+  check(dsg_model_info(dm.h, &n, &it, &adam_steps));
+  std::vector<double> p(14 * static_cast<size_t>(n));
   int32_t op = -1;
-  check(dsg_model_download(ctx.get(), dm.h, p.data(), static_cast<int64_t>(input.size()), &n, &it,
-                           &op));
+  check(dsg_model_download(ctx.get(), dm.h, p.data(), n, &n, &it, &op));
   detail::params_to(p, result.model);
   result.model.iteration = it;
   result.size_after_densify = result.model.size();
@@ -379,6 +384,52 @@ inline std::vector<double> knn_mean_distances(const PointCloud& pc, int k) {
     check(dsg_knn_mean(Context::current().get(), pts.data(), static_cast<int64_t>(pc.size()), k,
                        out.data()));
   return out;
+}
+
+// partition_cloud (partition.hpp:42-104): cuts, owned boxes and ownership /
+// ghost lists computed on the device in fp64 (bit-identical to the
+// reference); the point subsets are gathered here from the caller's cloud.
+inline std::vector<Partition> partition_cloud(const PointCloud& pc, int n, double ghost_margin) {
+  const auto pos = pc.positions();
+  std::vector<double> pts(3 * pos.size());
+  for (size_t i = 0; i < pos.size(); ++i) {
+    pts[3 * i] = pos[i].x;
+    pts[3 * i + 1] = pos[i].y;
+    pts[3 * i + 2] = pos[i].z;
+  }
+  const size_t k = n > 0 ? static_cast<size_t>(n) : 1;
+  int32_t axis = 0;
+  std::vector<double> lo(k), hi(k), box(6 * k);
+  std::vector<int64_t> oc(k), gc(k);
+  dsg_ctx ctx = Context::current().get();
+  const int64_t np = static_cast<int64_t>(pos.size());
+  check(dsg_partition(ctx, pts.data(), np, n, ghost_margin, &axis, lo.data(), hi.data(), box.data(),
+                      oc.data(), gc.data(), nullptr, nullptr, 0));  // size query
+  int64_t gtot = 0;
+  for (int64_t g : gc) gtot += g;
+  const int64_t cap = std::max<int64_t>({np, gtot, 1});
+  std::vector<uint32_t> oi(cap), gi(cap);
+  check(dsg_partition(ctx, pts.data(), np, n, ghost_margin, &axis, lo.data(), hi.data(), box.data(),
+                      oc.data(), gc.data(), oi.data(), gi.data(), cap));
+  std::vector<Partition> parts(k);
+  size_t o = 0, g = 0;
+  for (size_t j = 0; j < k; ++j) {
+    Partition& p = parts[j];
+    p.id = static_cast<int>(j);
+    p.ghost_margin = ghost_margin;
+    p.cut_axis = axis;
+    p.cut_lo = lo[j];
+    p.cut_hi = hi[j];
+    p.owned_box.lo = {box[6 * j], box[6 * j + 1], box[6 * j + 2]};
+    p.owned_box.hi = {box[6 * j + 3], box[6 * j + 4], box[6 * j + 5]};
+    p.owned_indices.assign(oi.begin() + o, oi.begin() + o + oc[j]);
+    p.ghost_indices.assign(gi.begin() + g, gi.begin() + g + gc[j]);
+    for (uint32_t x : p.owned_indices) p.owned_points.points.push_back(pc.points[x]);
+    for (uint32_t x : p.ghost_indices) p.ghost_points.points.push_back(pc.points[x]);
+    o += oc[j];
+    g += gc[j];
+  }
+  return parts;
 }
 
 }  // namespace dsplat::b200

@@ -486,6 +486,21 @@ def launch_count() -> int:
     return int(L.dsg_launch_count())
 
 
+class nvtx_range:
+    """NVTX range (context manager) through libdsg, for ncu --nvtx filtering."""
+
+    def __init__(self, name: str):
+        self.name = name.encode()
+
+    def __enter__(self):
+        lib().dsg_nvtx_push(C.c_char_p(self.name))
+        return self
+
+    def __exit__(self, *exc):
+        lib().dsg_nvtx_pop()
+        return False
+
+
 def frame_stats(ctx: Context):
     nv, nd = C.c_int64(), C.c_int64()
     _check(lib().dsg_frame_stats(ctx.h, C.byref(nv), C.byref(nd)))
@@ -520,7 +535,13 @@ def partition_cloud(positions, n: int, ghost_margin: float, ctx: Context = None)
     ax = C.c_int32()
     lo, hi, box = np.zeros(k), np.zeros(k), np.zeros((k, 6))
     oc, gc = np.zeros(k, np.int64), np.zeros(k, np.int64)
-    cap = max(1, npts * k)
+    cap = npts
+    if n > 1:  # ghost lists can exceed npts in total: size query first
+        _check(lib().dsg_partition(ctx.h, _p(pts), C.c_int64(npts), C.c_int32(n),
+                                   C.c_double(ghost_margin), C.byref(ax), _p(lo), _p(hi), _p(box),
+                                   _p(oc, C.c_int64), _p(gc, C.c_int64), None, None, C.c_int64(0)))
+        cap = max(npts, int(gc.sum()))
+    cap = max(cap, 1)
     oi, gi = np.zeros(cap, np.uint32), np.zeros(cap, np.uint32)
     _check(lib().dsg_partition(ctx.h, _p(pts), C.c_int64(npts), C.c_int32(n),
                                C.c_double(ghost_margin), C.byref(ax), _p(lo), _p(hi), _p(box),

@@ -14,6 +14,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/dsg.h"
 #include "dsg_internal.h"
 #include "raster.h"
@@ -1045,6 +1047,15 @@ int dsg_ground_truth_model(dsg_ctx ctx, const double* points, const double* colo
 
 int64_t dsg_launch_count(void) { return g_launches.load(); }
 
+int dsg_nvtx_push(const char* name) {
+  nvtxRangePushA(name ? name : "dsg");
+  return 0;
+}
+int dsg_nvtx_pop(void) {
+  nvtxRangePop();
+  return 0;
+}
+
 int dsg_frame_stats(dsg_ctx ctx, int64_t* n_visible, int64_t* n_dup) {
   return guarded([&] {
     if (n_visible) *n_visible = ctx->frame.n_visible;
@@ -1099,6 +1110,7 @@ int dsg_partition(dsg_ctx ctx, const double* positions, int64_t n, int32_t npart
       for (int c = 0; c < 6; ++c) owned_box[6 * k + c] = r.box[6 * k + c];
       owned_count[k] = (int64_t)r.owned[k].size();
       ghost_count[k] = (int64_t)r.ghost[k].size();
+      if (!owned_idx || !ghost_idx) continue;  // size query
       for (uint32_t x : r.owned[k]) {
         if (oi < cap) owned_idx[oi] = x;
         ++oi;
@@ -1108,7 +1120,8 @@ int dsg_partition(dsg_ctx ctx, const double* positions, int64_t n, int32_t npart
         ++gi;
       }
     }
-    if (oi > cap || gi > cap) fail(kInvalidArgument, "index capacity too small");
+    if (owned_idx && ghost_idx && (oi > cap || gi > cap))
+      fail(kInvalidArgument, "index capacity too small");
   });
 }
 

@@ -122,6 +122,59 @@ int main() {
            ra.final_loss, rb.final_loss);
     EXPECT(rb.model.iteration == init.iteration + 20, "iteration %ld", (long)rb.model.iteration);
   }
+  // densification resizes the model on the device; the drop-in returns it whole
+  {
+    Camera c = cam(32);
+    SplatModel init = scene(45, 8, 1.0);
+    init.gaussians[0].log_scale = {f32(std::log(0.5)), f32(std::log(0.35)), f32(std::log(0.25))};
+    init.gaussians[1].opacity_logit = -9.0;
+    TrainView v;
+    v.cam = c;
+    v.ground_truth = render(scene(46, 8, 1.0), c, cfg).color;
+    v.mask = Image(32, 32, 1, 1.0);
+    TrainConfig tc;
+    tc.iterations = 60;
+    tc.seed = 4;
+    tc.densify_interval = 10;
+    tc.densify_grad_threshold = 1e-5;
+    tc.split_scale_threshold = 0.2;
+    TrainResult ra = train_partition_full(init, {v}, tc);
+    TrainResult rb = b200::train_partition_full(init, {v}, tc);
+    EXPECT(ra.model.size() == rb.model.size() && rb.model.size() != init.size(),
+           "densified size %zu vs %zu", ra.model.size(), rb.model.size());
+    EXPECT(rb.size_after_densify == rb.model.size(), "size_after_densify");
+  }
+  // partition_cloud: bit-identical cuts, boxes and lists
+  {
+    Rng rng(77);
+    PointCloud pc;
+    for (int i = 0; i < 3000; ++i) {
+      SurfacePoint p;
+      p.position = {rng.uniform(-1, 1), rng.uniform(-0.5, 0.5), rng.uniform(-2, 2)};
+      if (i % 17 == 0) p.position.z = 0.25;  // ties on the cut axis
+      pc.points.push_back(p);
+    }
+    for (int n : {1, 3, 8}) {
+      auto a = partition_cloud(pc, n, 0.1);
+      auto b = b200::partition_cloud(pc, n, 0.1);
+      EXPECT(a.size() == b.size(), "partition count");
+      for (size_t k = 0; k < a.size() && k < b.size(); ++k) {
+        EXPECT(a[k].cut_axis == b[k].cut_axis && a[k].cut_lo == b[k].cut_lo &&
+                   a[k].cut_hi == b[k].cut_hi, "cuts %d/%zu", n, k);
+        EXPECT(a[k].owned_indices == b[k].owned_indices, "owned %d/%zu", n, k);
+        EXPECT(a[k].ghost_indices == b[k].ghost_indices, "ghosts %d/%zu", n, k);
+        EXPECT(a[k].owned_box.lo == b[k].owned_box.lo && a[k].owned_box.hi == b[k].owned_box.hi,
+               "box %d/%zu", n, k);
+        EXPECT(a[k].owned_points.size() == b[k].owned_points.size(), "owned points %d/%zu", n, k);
+      }
+    }
+    try {
+      b200::partition_cloud(PointCloud{}, 2, 0.1);
+      EXPECT(false, "EmptyCloud not thrown");
+    } catch (const Error& e) {
+      EXPECT(e.code() == ErrorCode::EmptyCloud, "code %d", (int)e.code());
+    }
+  }
   std::printf("dropin_parity: %d failure(s)\n", failures);
   return failures;
 }
