@@ -239,6 +239,11 @@ int dsg_host_unregister(void* ptr);
 int dsg_nvtx_push(const char* name);
 int dsg_nvtx_pop(void);
 
+/* Blend sub-tile masks from exact per-row coverage (1, default) or from the
+ * effective rect alone (0). Both give identical results; 0 exists so the
+ * parity tests can prove that. Process-wide. */
+int dsg_set_exact_masks(int32_t enable);
+
 /* Record per-stage CUDA events inside dsg_train (adds one sync per step). */
 int dsg_set_profiling(dsg_ctx ctx, int32_t enable);
 

@@ -486,6 +486,11 @@ def launch_count() -> int:
     return int(L.dsg_launch_count())
 
 
+def set_exact_masks(enable: bool):
+    """Sub-tile masks from exact row coverage (default) or the rect only."""
+    _check(lib().dsg_set_exact_masks(C.c_int32(1 if enable else 0)))
+
+
 class nvtx_range:
     """NVTX range (context manager) through libdsg, for ncu --nvtx filtering."""
 

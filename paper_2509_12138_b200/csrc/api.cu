@@ -890,6 +890,11 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
   });
 }
 
+int dsg_set_exact_masks(int32_t enable) {
+  g_exact_masks.store(enable != 0);
+  return 0;
+}
+
 int dsg_set_profiling(dsg_ctx ctx, int32_t enable) {
   return guarded([&] { ctx->profile = enable != 0; });
 }

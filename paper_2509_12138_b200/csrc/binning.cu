@@ -12,6 +12,8 @@
 // — the reference comparator (render.hpp:98-101) — and the duplicates are
 // then stably sorted by tile id, so every tile list is in reference
 // compositing order.
+#include <atomic>
+
 #include "dsg_internal.h"
 #include "raster.h"
 #include "scan_util.cuh"
@@ -150,12 +152,75 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv
   if (s < nv) out[s] = tcount[vis_idx[s]];
 }
 
+// Sub-tile mask of one (splat, tile): bit (sy*2 + sx) for every 8x4 sub-tile
+// holding a pixel centre the splat can composite at. Compositing needs
+// q <= sigma^2 and o*exp(-q/2) >= alpha_cutoff (render.hpp:140-154), i.e.
+// q <= q_eff = min(sigma^2, 2 ln(o/alpha_cutoff)); the blend's fp32 path
+// agrees with fp64 on every such decision (guard band), so the composited
+// set is the fp64 one. With q = ixx (dx - dx*)^2 + q0 dy^2, each pixel row's
+// q <= qcut set is the x interval centred at dx* = -ixy dy / ixx with
+// half-width sqrt((qcut - q0 dy^2) / ixx). Per splat the constants come from
+// the fp64 values (qcut = q_eff + 1e-9 relative); per row they are evaluated
+// in fp32 (mean2d as hi/lo pairs, so dy is exact to ~1e-7 relative) with the
+// half-width squared padded by 1e-5 of its maximum and the interval widened
+// by 2e-3 px plus 1e-5 relative — well above the fp32 rounding (about 1e-6
+// of q) — then intersected with the effective rect (itself
+// widened by a pixel). A cleared bit therefore never hides a composited
+// pixel, and the blend warps skip the (entry, sub-tile) hits the rect test
+// alone would admit.
+constexpr int kMaskShift = 24;  // tile keys carry the mask above the tile id
+constexpr uint32_t kTileIdMask = (1u << kMaskShift) - 1u;
+
+struct MaskSplat {
+  int4 er;                   // effective rect (pixels, widened by one)
+  float mx, my, mxl, myl;    // mean2d as hi/lo pairs (dy must be accurate: q ~ q0 dy^2)
+  float r, inv_ixx, q0;      // ixy / ixx, 1 / ixx, iyy - ixy^2 / ixx
+  float qcut, pad;           // q threshold; 1e-5 * qcut / ixx
+};
+
+// rows = false: effective-rect test only (dsg_set_exact_masks; the parity
+// tests check the two give bit-identical renders and gradients)
+__device__ __forceinline__ uint32_t subtile_mask(const MaskSplat& sp, int ox, int oy, bool rows) {
+  const int ry0 = max(sp.er.y, oy), ry1 = min(sp.er.w, oy + kTile - 1);
+  const int cx0 = max(sp.er.x, ox), cx1 = min(sp.er.z, ox + kTile - 1);
+  uint32_t m = 0;
+  if (cx0 > cx1) return 0;
+  if (!rows) {
+    for (int y = ry0; y <= ry1; ++y) {
+      const int sy = (y - oy) >> 2;
+      if (cx0 < ox + 8) m |= 1u << (sy * 2);
+      if (cx1 >= ox + 8) m |= 1u << (sy * 2 + 1);
+    }
+    return m;
+  }
+  for (int y = ry0; y <= ry1; ++y) {
+    const float dy = (((float)y + 0.5f) - sp.my) - sp.myl;
+    const float h2 = (sp.qcut - dy * dy * sp.q0) * sp.inv_ixx + sp.pad;
+    if (h2 < 0.f) continue;
+    const float c = (sp.mx - sp.r * dy) + sp.mxl;  // x of the row's minimum q
+    const float h = sqrtf(h2);
+    const float eps = 2e-3f + 1e-5f * (fabsf(c) + h);
+    // pixel x (centre x + 0.5) with centre in [c - h - eps, c + h + eps]
+    const float lo = ceilf(c - h - eps - 0.5f), hi = floorf(c + h + eps - 0.5f);
+    const int xl = lo < (float)cx0 ? cx0 : (int)lo;
+    const int xh = hi > (float)cx1 ? cx1 : (int)hi;
+    if (xl > xh) continue;
+    const int sy = (y - oy) >> 2;
+    if (xl < ox + 8) m |= 1u << (sy * 2);
+    if (xh >= ox + 8) m |= 1u << (sy * 2 + 1);
+  }
+  return m;
+}
+
 // K2: one (tile id, gaussian index) pair per overlapped tile, emitted in
 // depth order; tile enumeration row-major inside the rect (render.hpp:127-133).
+// The key's high byte carries the entry's sub-tile mask through the tile sort
+// (the sort only ranks the tile-id bits).
 __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
                             const uint32_t* __restrict__ offs, const int4* __restrict__ trect,
-                            int tiles_x, int band_ty0, int band_ty1,
-                            uint32_t* __restrict__ tile_key,
+                            const int4* __restrict__ erect, const double2* __restrict__ exact,
+                            double sig2, double acut, bool rows, int tiles_x, int band_ty0,
+                            int band_ty1, uint32_t* __restrict__ tile_key,
                             uint32_t* __restrict__ dup_val, uint32_t* __restrict__ dup_base) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nv) return;
@@ -163,44 +228,47 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
   uint32_t o = offs[s];
   dup_base[i] = o;
   const int4 pr = trect[i];
+  MaskSplat ms;
+  ms.er = erect[i];
+  {
+    const double2* ex = exact + 3 * (size_t)i;
+    const double2 e0 = ex[0], e1 = ex[1], e2 = ex[2];
+    const double inv = 1.0 / e1.x, r = e1.y * inv;
+    const double qe = fmin(sig2, 2.0 * log(e2.y / acut));
+    const double qc = qe + 1e-9 * fabs(qe) + 1e-12;
+    ms.mx = (float)e0.x;
+    ms.my = (float)e0.y;
+    ms.mxl = (float)(e0.x - (double)ms.mx);
+    ms.myl = (float)(e0.y - (double)ms.my);
+    ms.r = (float)r;
+    ms.inv_ixx = (float)inv;
+    ms.q0 = (float)(e2.x - e1.y * r);
+    ms.qcut = (float)qc;
+    ms.pad = (float)(1e-5 * fabs(qc) * inv);
+  }
   const int4 r = make_int4(pr.x / kTile, max(pr.y / kTile, band_ty0), pr.z / kTile,
                            min(pr.w / kTile, band_ty1 - 1));
   for (int ty = r.y; ty <= r.w; ++ty)
     for (int tx = r.x; tx <= r.z; ++tx) {
-      tile_key[o] = (uint32_t)(ty * tiles_x + tx);
+      const uint32_t m = subtile_mask(ms, tx * kTile, ty * kTile, rows);
+      tile_key[o] = (uint32_t)(ty * tiles_x + tx) | (m << kMaskShift);
       dup_val[o] = i;
       ++o;
     }
 }
 
-// K4: [start, end) of every tile in the sorted duplicate list.
-// Per sorted entry, the 8x4 sub-tiles of its tile that its pixel rect
-// (widened by one pixel) touches: bit (sy*2 + sx). Lets each blend warp skip
-// entries that cannot reach its pixels from one coalesced byte read.
-__global__ void k_entry_masks(const uint32_t* __restrict__ tile_key,
-                              const uint32_t* __restrict__ val, const int4* __restrict__ prect,
-                              int64_t nd, int tiles_x, uint8_t* __restrict__ mask) {
+// K4: [start, end) of every tile in the sorted duplicate list, and the
+// entries' sub-tile masks split off the keys (one coalesced byte per entry
+// for the blend warps).
+__global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd, uint2* ranges,
+                              uint8_t* __restrict__ emask) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= nd) return;
-  const uint32_t t = tile_key[e];
-  const int4 pr = prect[val[e]];  // effective rect, already widened by one pixel
-  const int ox = (int)(t % (uint32_t)tiles_x) * kTile, oy = (int)(t / (uint32_t)tiles_x) * kTile;
-  const int x0 = pr.x - ox, x1 = pr.z - ox, y0 = pr.y - oy, y1 = pr.w - oy;
-  uint32_t m = 0;
-#pragma unroll
-  for (int w = 0; w < 8; ++w) {
-    const int cx0 = (w & 1) * 8, cy0 = (w >> 1) * 4;
-    if (x0 <= cx0 + 7 && x1 >= cx0 && y0 <= cy0 + 3 && y1 >= cy0) m |= 1u << w;
-  }
-  mask[e] = (uint8_t)m;
-}
-
-__global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd, uint2* ranges) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nd) return;
-  uint32_t t = tile_key[e];
-  if (e == 0 || tile_key[e - 1] != t) ranges[t].x = (uint32_t)e;
-  if (e == nd - 1 || tile_key[e + 1] != t) ranges[t].y = (uint32_t)(e + 1);
+  const uint32_t k = tile_key[e];
+  const uint32_t t = k & kTileIdMask;
+  emask[e] = (uint8_t)(k >> kMaskShift);
+  if (e == 0 || (tile_key[e - 1] & kTileIdMask) != t) ranges[t].x = (uint32_t)e;
+  if (e == nd - 1 || (tile_key[e + 1] & kTileIdMask) != t) ranges[t].y = (uint32_t)(e + 1);
 }
 
 // Longest-first tile schedule for the blend kernels: tiles are bucketed by
@@ -238,6 +306,8 @@ __global__ void k_tile_order(const uint32_t* __restrict__ bins, int t0, int nt, 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
+
+std::atomic<int> g_exact_masks{1};
 
 void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
                const RenderDev& rd, cudaStream_t st, StageTimer* timer) {
@@ -319,10 +389,14 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.dup_val.ensure(std::max<uint32_t>(nd, 1));
   f.tile_key2.ensure(std::max<uint32_t>(nd, 1));
   f.dup_val2.ensure(std::max<uint32_t>(nd, 1));
-  k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(), cam.tiles_x,
-                                               cam.band_ty0, cam.band_ty1, f.tile_key.get(),
-                                               f.dup_val.get(), f.dup_base.get());
-                                               count_launch();
+  if (f.tiles > (int64_t)kTileIdMask) fail(kInvalidArgument, "image has too many tiles");
+  k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(),
+                                               f.erect.get(), f.exact.get(), rd.sigma_sq,
+                                               rd.alpha_cutoff, g_exact_masks.load() != 0,
+                                               cam.tiles_x, cam.band_ty0, cam.band_ty1,
+                                               f.tile_key.get(), f.dup_val.get(),
+                                               f.dup_base.get());
+  count_launch();
   tm.mark(3, st);
   int tile_bits = 1;
   while ((int64_t(1) << tile_bits) < f.tiles) ++tile_bits;
@@ -330,11 +404,9 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
                                           f.dup_val2.get(), nd, 0, tile_bits, f.sort, st);
   f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
   f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
-  k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get());
-  count_launch();
   f.emask.ensure(std::max<uint32_t>(nd, 1));
-  k_entry_masks<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, f.sorted_val, f.erect.get(), nd,
-                                                 cam.tiles_x, f.emask.get());
+  k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get(),
+                                                 f.emask.get());
   count_launch();
   {
     const int t0 = cam.band_ty0 * cam.tiles_x;

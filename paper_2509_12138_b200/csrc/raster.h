@@ -1,5 +1,7 @@
 // Raster pipeline state for one view (per context scratch) and launchers.
 #pragma once
+#include <atomic>
+
 #include "dsg_internal.h"
 
 namespace dsg {
@@ -113,6 +115,8 @@ struct StageTimer {
   }
 };
 
+// Sub-tile masks from exact per-row coverage (1, default) or the rect only.
+extern std::atomic<int> g_exact_masks;
 void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
                const RenderDev& rd, cudaStream_t st, StageTimer* timer = nullptr);
 void blend_forward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,

@@ -163,3 +163,36 @@ def test_train_with_densify_matches_oracle(orc, ctx, split_thr):
     assert len(a.model) == len(b.model) and len(a.model) != len(init)
     np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=2e-3)
     np.testing.assert_allclose(a.model.params, b.model.params, rtol=0, atol=5e-3)
+
+
+@pytest.mark.parametrize("scene", ["kingsnake", "random"])
+def test_exact_submasks_change_nothing(ctx, scene):
+    """The exact per-row sub-tile masks only skip (entry, sub-tile) hits that
+    cannot composite: renders, contributor counts and gradients are
+    bit-identical to the rect-only masks."""
+    if scene == "kingsnake":
+        pts, cols, _ = scenes.kingsnake(300_000, seed=3)
+        model = api.seed_gaussians(pts, cols, 3, ctx=ctx).download()
+        cams = scenes.rig_for_cloud(pts, 8, 4, 384)[::7]
+    else:
+        model = fp32_exact(random_scene(71, 3000))
+        model.params[:, 3:6] += np.log(np.random.default_rng(5).uniform(0.05, 1.0, (3000, 3)))
+        model = fp32_exact(model)
+        cams = [make_camera(160)]
+    rc = RenderConfig()
+    outs = []
+    for exact in (True, False):
+        api.set_exact_masks(exact)
+        try:
+            res = []
+            for cam in cams:
+                r = api.render(model, cam, rc, ctx=ctx)
+                dl = np.random.default_rng(9).normal(size=r.color.shape)
+                g = api.backward(model, cam, rc, r, dl, ctx=ctx)
+                res.append((r.color, r.per_pixel_contributor_count, g.grads, g.touch_count))
+            outs.append(res)
+        finally:
+            api.set_exact_masks(True)
+    for a, b in zip(*outs):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
