@@ -367,9 +367,13 @@ def run_ours(args, dist: Dist):
     ctx.synchronize()
     e0 = time.perf_counter()
     dm_e.upload(SplatModel(host_params))
+    e1 = time.perf_counter()
     api.train_device(dm_e, hv, train_config(args, dist.rank, args.steps))
+    e2 = time.perf_counter()
     out = dm_e.download()
     e_wall = time.perf_counter() - e0
+    e_parts = {"upload_s": round(e1 - e0, 4), "train_s": round(e2 - e1, 4),
+               "download_s": round(e0 + e_wall - e2, 4)}
     e_max = dist.max(e_wall)
     view_bytes = npix * (3 * 4 + 1)
     h2d = view_bytes + n * 14 * 8 / args.steps
@@ -407,7 +411,8 @@ def run_ours(args, dist: Dist):
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "n_dup": n_dup,
         "e2e": {"value": round(total_iters / e_max, 3), "unit": "it/s",
-                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)},
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "breakdown": e_parts},
         "gpu_launches": int(dist.sum(float(launches))),
         "roofline": roof,
         "cpu_baseline": cpu,

@@ -187,11 +187,11 @@ class DeviceModel:
 
     def download(self) -> SplatModel:
         n, _, _ = self.info()
-        P = np.zeros((max(n, 1), PARAMS))
+        P = np.empty((max(n, 1), PARAMS))
         nn, it, op = C.c_int64(), C.c_int64(), C.c_int32()
         _check(lib().dsg_model_download(self.ctx.h, self.h, _p(P), C.c_int64(P.shape[0]),
                                         C.byref(nn), C.byref(it), C.byref(op)))
-        return SplatModel(P[: nn.value].copy(), it.value, None if op.value < 0 else op.value)
+        return SplatModel(P[: nn.value], it.value, None if op.value < 0 else op.value)
 
     def adam_state(self):
         n, _, _ = self.info()

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <nvtx3/nvToolsExt.h>
@@ -74,6 +75,13 @@ struct dsg_ctx_s {
   ModelDev spare;  // densification output storage (swapped with the model's)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   double* host_loss = nullptr;  // pinned, end-to-end mode
+  // end-to-end mode: next step's view is copied on its own stream into the
+  // other of two device slots while this step computes
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+  // pinned staging for large pageable model transfers (staged_copy)
+  char* pin[2] = {nullptr, nullptr};
+  cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   double last_total_ms = 0.0;
   int64_t last_iters = 0;
   double last_stage_ms[StageTimer::kStages] = {};
@@ -88,8 +96,8 @@ struct dsg_views_s {
   int32_t n = 0;
   int width = 0, height = 0;
   std::vector<dsg_camera> cams;
-  DevBuf<float> gt;       // [v][3][npix] (host mode: one staging slot)
-  DevBuf<uint8_t> mask;   // [v][npix]
+  DevBuf<float> gt;       // [v][3][npix] (host mode: two staging slots)
+  DevBuf<uint8_t> mask;   // [v][npix] (host mode: two slots)
   bool host = false;      // views live in caller-owned pinned host memory
   std::vector<const float*> host_gt;
   std::vector<const uint8_t*> host_mask;
@@ -380,6 +388,15 @@ int dsg_ctx_destroy(dsg_ctx ctx) {
       cudaEventDestroy(ctx->ev_end);
     }
     if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
+    for (int k = 0; k < 2; ++k) {
+      if (ctx->ev_copied[k]) cudaEventDestroy(ctx->ev_copied[k]);
+      if (ctx->ev_consumed[k]) cudaEventDestroy(ctx->ev_consumed[k]);
+    }
+    if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+    for (int k = 0; k < 2; ++k) {
+      if (ctx->pin[k]) cudaFreeHost(ctx->pin[k]);
+      if (ctx->pin_ev[k]) cudaEventDestroy(ctx->pin_ev[k]);
+    }
     cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -403,6 +420,69 @@ int dsg_model_destroy(dsg_model model) {
   return guarded([&] { delete model; });
 }
 
+namespace {
+
+// Copy between a large pageable host buffer and device memory: 32 MiB chunks
+// through two pinned staging buffers, the DMA of one chunk overlapping a
+// multi-threaded host memcpy of the other (a single pageable cudaMemcpy is
+// bound by the driver's one-thread staging copy and first-touch faults).
+void par_memcpy(char* dst, const char* src, size_t n) {
+  const size_t kMinPerThread = 1 << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>({(size_t)std::min(hw, 16u), (n + kMinPerThread - 1) / kMinPerThread});
+  if (nt <= 1) {
+    std::memcpy(dst, src, n);
+    return;
+  }
+  const size_t per = ((n + nt - 1) / nt + 4095) & ~size_t(4095);
+  std::vector<std::thread> th;
+  for (size_t o = 0; o < n; o += per)
+    th.emplace_back([=] { std::memcpy(dst + o, src + o, std::min(per, n - o)); });
+  for (auto& t : th) t.join();
+}
+
+void staged_copy(dsg_ctx ctx, char* host, char* dev, size_t bytes, bool to_host) {
+  constexpr size_t kChunk = size_t(32) << 20;
+  cudaStream_t st = ctx->stream;
+  if (bytes < (size_t(8) << 20)) {
+    DSG_CUDA_CHECK(cudaMemcpyAsync(to_host ? (void*)host : (void*)dev, to_host ? (void*)dev : (void*)host,
+                                   bytes, to_host ? cudaMemcpyDeviceToHost : cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    return;
+  }
+  for (int k = 0; k < 2; ++k) {
+    if (!ctx->pin[k]) DSG_CUDA_CHECK(cudaMallocHost(&ctx->pin[k], kChunk));
+    if (!ctx->pin_ev[k]) DSG_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->pin_ev[k], cudaEventDisableTiming));
+  }
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  auto len = [&](size_t k) { return std::min(kChunk, bytes - k * kChunk); };
+  if (to_host) {
+    DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->pin[0], dev, len(0), cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaEventRecord(ctx->pin_ev[0], st));
+    for (size_t k = 0; k < nch; ++k) {
+      if (k + 1 < nch) {  // its buffer's previous chunk (k-1) was drained last iteration
+        const int b = (int)((k + 1) & 1);
+        DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->pin[b], dev + (k + 1) * kChunk, len(k + 1),
+                                       cudaMemcpyDeviceToHost, st));
+        DSG_CUDA_CHECK(cudaEventRecord(ctx->pin_ev[b], st));
+      }
+      DSG_CUDA_CHECK(cudaEventSynchronize(ctx->pin_ev[k & 1]));
+      par_memcpy(host + k * kChunk, ctx->pin[k & 1], len(k));
+    }
+  } else {
+    for (size_t k = 0; k < nch; ++k) {
+      const int b = (int)(k & 1);
+      if (k >= 2) DSG_CUDA_CHECK(cudaEventSynchronize(ctx->pin_ev[b]));  // buffer's DMA done
+      par_memcpy(ctx->pin[b], host + k * kChunk, len(k));
+      DSG_CUDA_CHECK(cudaMemcpyAsync(dev + k * kChunk, ctx->pin[b], len(k), cudaMemcpyHostToDevice, st));
+      DSG_CUDA_CHECK(cudaEventRecord(ctx->pin_ev[b], st));
+    }
+  }
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
+}  // namespace
+
 int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t n,
                      int64_t iteration, int32_t origin_partition) {
   return guarded([&] {
@@ -415,8 +495,8 @@ int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t
     m.origin_partition = origin_partition;
     if (n > 0) {
       double* st = ctx->stage_d.ensure(kParams * n);
-      DSG_CUDA_CHECK(cudaMemcpyAsync(st, params, sizeof(double) * kParams * n, cudaMemcpyHostToDevice,
-                                     ctx->stream));
+      staged_copy(ctx, (char*)const_cast<double*>(params), (char*)st, sizeof(double) * kParams * n,
+                  false);
       k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
       count_launch();
     }
@@ -434,8 +514,8 @@ int dsg_model_set_params(dsg_ctx ctx, dsg_model model, const double* params, int
     m.iteration = iteration;
     if (n > 0) {
       double* st = ctx->stage_d.ensure(kParams * n);
-      DSG_CUDA_CHECK(cudaMemcpyAsync(st, params, sizeof(double) * kParams * n, cudaMemcpyHostToDevice,
-                                     ctx->stream));
+      staged_copy(ctx, (char*)const_cast<double*>(params), (char*)st, sizeof(double) * kParams * n,
+                  false);
       k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
       count_launch();
     }
@@ -456,9 +536,7 @@ int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t cap
     double* st = ctx->stage_d.ensure(kParams * m.n);
     k_planar_to_aos<<<nblk(m.n), 256, 0, ctx->stream>>>(m.params.get(), m.cap, m.n, kParams, st);
     count_launch();
-    DSG_CUDA_CHECK(cudaMemcpyAsync(params, st, sizeof(double) * kParams * m.n, cudaMemcpyDeviceToHost,
-                                   ctx->stream));
-    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    staged_copy(ctx, (char*)params, (char*)st, sizeof(double) * kParams * m.n, true);
   });
 }
 
@@ -741,8 +819,8 @@ int dsg_views_create_host(dsg_ctx ctx, const dsg_camera* cams, const float* cons
       }
       DeviceGuard g(ctx->device);
       const int64_t npix = (int64_t)v->width * v->height;
-      v->gt.ensure(std::max<int64_t>(1, 3 * npix));
-      v->mask.ensure(std::max<int64_t>(1, npix));
+      v->gt.ensure(std::max<int64_t>(1, 2 * 3 * npix));
+      v->mask.ensure(std::max<int64_t>(1, 2 * npix));
     } catch (...) {
       delete v;
       throw;
@@ -798,18 +876,41 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     double stage[StageTimer::kStages] = {};
     if (views->host && !ctx->host_loss) {
       DSG_CUDA_CHECK(cudaMallocHost(&ctx->host_loss, sizeof(double)));
+      DSG_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      for (int k = 0; k < 2; ++k) {
+        DSG_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_copied[k], cudaEventDisableTiming));
+        DSG_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_consumed[k], cudaEventDisableTiming));
+      }
     }
+    // end-to-end mode: views come from pinned host memory, double-buffered
+    // so the copy of step it+1 overlaps step it (slot reuse waits for the
+    // loss of step it-1, the last reader of that slot)
+    auto copy_view = [&](int64_t step) {
+      const size_t v = order[(size_t)step % order.size()];
+      const int slot = (int)(step & 1);
+      cudaStream_t cs = ctx->copy_stream;
+      DSG_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_consumed[slot], 0));
+      DSG_CUDA_CHECK(cudaMemcpyAsync(views->gt.get() + 3 * npix * slot, views->host_gt[v],
+                                     sizeof(float) * 3 * npix, cudaMemcpyHostToDevice, cs));
+      DSG_CUDA_CHECK(cudaMemcpyAsync(views->mask.get() + npix * slot, views->host_mask[v], npix,
+                                     cudaMemcpyHostToDevice, cs));
+      DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_copied[slot], cs));
+    };
     DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_begin, st));
+    if (views->host) {
+      // slots are free once the previous call's stream work is done
+      for (int k = 0; k < 2; ++k) DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_consumed[k], st));
+      copy_view(0);
+    }
     for (int64_t it = 0; it < iters; ++it) {
       const size_t vi = order[(size_t)it % order.size()];
       const CamDev& cam = cams[vi];
-      const float* gt = views->gt.get() + (views->host ? 0 : 3 * npix * vi);
-      const uint8_t* mk = views->mask.get() + (views->host ? 0 : npix * vi);
-      if (views->host) {  // end-to-end mode: this step's view comes from pinned host memory
-        DSG_CUDA_CHECK(cudaMemcpyAsync(views->gt.get(), views->host_gt[vi], sizeof(float) * 3 * npix,
-                                       cudaMemcpyHostToDevice, st));
-        DSG_CUDA_CHECK(cudaMemcpyAsync(views->mask.get(), views->host_mask[vi], npix,
-                                       cudaMemcpyHostToDevice, st));
+      const int slot = (int)(it & 1);
+      const float* gt = views->gt.get() + 3 * npix * (views->host ? (size_t)slot : vi);
+      const uint8_t* mk = views->mask.get() + npix * (views->host ? (size_t)slot : vi);
+      if (views->host) {
+        DSG_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copied[slot], 0));
+        if (it + 1 < iters) copy_view(it + 1);
       }
       bin_frame(ctx->frame, m.params.get(), m.cap, m.n, cam, rd, st, &tm);
       Frame& f = ctx->frame;
@@ -824,9 +925,11 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
       masked_loss_dev(f, gt, mk, views->width, views->height, cfg->loss_lambda, st);
       DSG_CUDA_CHECK(cudaMemcpyAsync(trace + it, f.loss_out.get(), sizeof(double),
                                      cudaMemcpyDeviceToDevice, st));
-      if (views->host)  // the step's result read back to the host
+      if (views->host) {  // the step's result read back to the host; view slot free
+        DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_consumed[slot], st));
         DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->host_loss, f.loss_out.get(), sizeof(double),
                                        cudaMemcpyDeviceToHost, st));
+      }
       tm.mark(6, st);
       if (!empty) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
       tm.mark(7, st);
@@ -843,7 +946,7 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
         a.tcount = f.tcount.get();
         a.dup_base = f.dup_base.get();
         a.partials = f.partials.get();
-  a.tmask = f.tmask.get();
+        a.tmask = f.tmask.get();
         a.grads = m.grads.get();
         a.dmean = m.dmean.get();
         a.touch = m.touch.get();
