@@ -75,10 +75,13 @@ struct ScanScratch {
 // ends in the *_alt buffers. Digits whose histogram is a single bin are
 // skipped (stable no-op). Synchronizes the stream once (histogram readback).
 // Digits are taken from (key - offset), so a key range known to start at
-// `offset` needs only end_bit = bit-length(max - offset) bits.
+// `offset` needs only end_bit = bit-length(max - offset) bits. With
+// skip_trivial = false every pass runs and the call never synchronizes
+// (the per-step sorts, whose digits all vary).
 template <class K>
 bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
-                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset = 0);
+                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset = 0,
+                      bool skip_trivial = true);
 
 // Exclusive prefix sum of n u32 into out (out[n] = total). out may alias in.
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratch& s,

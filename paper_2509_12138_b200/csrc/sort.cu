@@ -306,7 +306,8 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratc
 
 template <class K>
 bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
-                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset) {
+                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset,
+                      bool skip_trivial) {
   if (n <= 1 || end_bit <= begin_bit) return false;
   if (n > (int64_t)kValueMask) fail(kInvalidArgument, "radix sort: too many keys");
   const int passes = (end_bit - begin_bit + kRadixBits - 1) / kRadixBits;
@@ -321,14 +322,16 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
   k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, offset, hist);
   count_launch();
   // Which digits actually vary? (a single populated bin = identity pass)
-  s.host_hist.resize((size_t)passes * kRadix);
-  DSG_CUDA_CHECK(cudaMemcpyAsync(s.host_hist.data(), hist, sizeof(uint32_t) * passes * kRadix,
-                                 cudaMemcpyDeviceToHost, st));
-  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
   std::vector<bool> trivial(passes, false);
-  for (int p = 0; p < passes; ++p)
-    for (int d = 0; d < kRadix; ++d)
-      if (s.host_hist[(size_t)p * kRadix + d] == (uint32_t)n) trivial[p] = true;
+  if (skip_trivial) {
+    s.host_hist.resize((size_t)passes * kRadix);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(s.host_hist.data(), hist, sizeof(uint32_t) * passes * kRadix,
+                                   cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (int p = 0; p < passes; ++p)
+      for (int d = 0; d < kRadix; ++d)
+        if (s.host_hist[(size_t)p * kRadix + d] == (uint32_t)n) trivial[p] = true;
+  }
   k_hist_scan<<<passes, kRadix, 0, st>>>(hist);
   count_launch();
   const size_t smem = sizeof(OnesweepSmem<K>);
@@ -352,8 +355,8 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
 }
 
 template bool radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t, int,
-                                         int, SortScratch&, cudaStream_t, uint32_t);
+                                         int, SortScratch&, cudaStream_t, uint32_t, bool);
 template bool radix_sort_pairs<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, int64_t, int,
-                                         int, SortScratch&, cudaStream_t, uint64_t);
+                                         int, SortScratch&, cudaStream_t, uint64_t, bool);
 
 }  // namespace dsg
