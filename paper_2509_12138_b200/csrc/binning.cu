@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
         // o*exp(-q/2) >= c, i.e. q <= 2 ln(o/c), so only pixels with
         // |d| <= sqrt(q_eff * cov) can composite (widened by one pixel).
         const double q_eff = fmin(a.rd.sigma_sq, 2.0 * log(op / a.rd.alpha_cutoff));
+        {  // sub-tile mask constants (see subtile_mask): ixy/ixx, 1/ixx, q0, qcut
+          const double inv = 1.0 / ixx, rr = ixy * inv;
+          a.mrow[i] = make_float4((float)rr, (float)inv, (float)(iyy - ixy * rr),
+                                  (float)(q_eff + 1e-9 * fabs(q_eff) + 1e-12));
+        }
         if (q_eff < 0.0) {
           a.erect[i] = make_int4(1, 1, 0, 0);  // never composites anywhere
         } else {
@@ -159,8 +164,8 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv
 // agrees with fp64 on every such decision (guard band), so the composited
 // set is the fp64 one. With q = ixx (dx - dx*)^2 + q0 dy^2, each pixel row's
 // q <= qcut set is the x interval centred at dx* = -ixy dy / ixx with
-// half-width sqrt((qcut - q0 dy^2) / ixx). Per splat the constants come from
-// the fp64 values (qcut = q_eff + 1e-9 relative); per row they are evaluated
+// half-width sqrt((qcut - q0 dy^2) / ixx). Per splat the constants are
+// formed by K1 from the fp64 values (qcut = q_eff + 1e-9 relative); per row they are evaluated
 // in fp32 (mean2d as hi/lo pairs, so dy is exact to ~1e-7 relative) with the
 // half-width squared padded by 1e-5 of its maximum and the interval widened
 // by 2e-3 px plus 1e-5 relative — well above the fp32 rounding (about 1e-6
@@ -218,8 +223,8 @@ __device__ __forceinline__ uint32_t subtile_mask(const MaskSplat& sp, int ox, in
 // (the sort only ranks the tile-id bits).
 __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
                             const uint32_t* __restrict__ offs, const int4* __restrict__ trect,
-                            const int4* __restrict__ erect, const double2* __restrict__ exact,
-                            double sig2, double acut, bool rows, int tiles_x, int band_ty0,
+                            const int4* __restrict__ erect, const float4* __restrict__ rec,
+                            const float4* __restrict__ mrow, bool rows, int tiles_x, int band_ty0,
                             int band_ty1, uint32_t* __restrict__ tile_key,
                             uint32_t* __restrict__ dup_val, uint32_t* __restrict__ dup_base) {
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -231,20 +236,16 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
   MaskSplat ms;
   ms.er = erect[i];
   {
-    const double2* ex = exact + 3 * (size_t)i;
-    const double2 e0 = ex[0], e1 = ex[1], e2 = ex[2];
-    const double inv = 1.0 / e1.x, r = e1.y * inv;
-    const double qe = fmin(sig2, 2.0 * log(e2.y / acut));
-    const double qc = qe + 1e-9 * fabs(qe) + 1e-12;
-    ms.mx = (float)e0.x;
-    ms.my = (float)e0.y;
-    ms.mxl = (float)(e0.x - (double)ms.mx);
-    ms.myl = (float)(e0.y - (double)ms.my);
-    ms.r = (float)r;
-    ms.inv_ixx = (float)inv;
-    ms.q0 = (float)(e2.x - e1.y * r);
-    ms.qcut = (float)qc;
-    ms.pad = (float)(1e-5 * fabs(qc) * inv);
+    const float4 m0 = __ldg(rec + 3 * (size_t)i), k = __ldg(mrow + i);
+    ms.mx = m0.x;
+    ms.my = m0.y;
+    ms.mxl = m0.z;
+    ms.myl = m0.w;
+    ms.r = k.x;
+    ms.inv_ixx = k.y;
+    ms.q0 = k.z;
+    ms.qcut = k.w;
+    ms.pad = 1e-5f * fabsf(k.w) * k.y;
   }
   const int4 r = make_int4(pr.x / kTile, max(pr.y / kTile, band_ty0), pr.z / kTile,
                            min(pr.w / kTile, band_ty1 - 1));
@@ -319,6 +320,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.rec.ensure(3 * (size_t)std::max<int64_t>(n, 1));
   f.trect.ensure(std::max<int64_t>(n, 1));
   f.erect.ensure(std::max<int64_t>(n, 1));
+  f.mrow.ensure(std::max<int64_t>(n, 1));
   f.tcount.ensure(std::max<int64_t>(n, 1));
   f.depth.ensure(std::max<int64_t>(n, 1));
   f.exact.ensure(3 * (size_t)std::max<int64_t>(n, 1));
@@ -345,6 +347,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     a.rec = f.rec.get();
     a.trect = f.trect.get();
     a.erect = f.erect.get();
+    a.mrow = f.mrow.get();
     a.tcount = f.tcount.get();
     a.depth = f.depth.get();
     a.exact = f.exact.get();
@@ -391,8 +394,8 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.dup_val2.ensure(std::max<uint32_t>(nd, 1));
   if (f.tiles > (int64_t)kTileIdMask) fail(kInvalidArgument, "image has too many tiles");
   k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(),
-                                               f.erect.get(), f.exact.get(), rd.sigma_sq,
-                                               rd.alpha_cutoff, g_exact_masks.load() != 0,
+                                               f.erect.get(), f.rec.get(), f.mrow.get(),
+                                               g_exact_masks.load() != 0,
                                                cam.tiles_x, cam.band_ty0, cam.band_ty1,
                                                f.tile_key.get(), f.dup_val.get(),
                                                f.dup_base.get());

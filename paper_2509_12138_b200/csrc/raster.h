@@ -14,6 +14,7 @@ struct PreprocessArgs {
   float4* rec;          // [n][3] blend payload (model order)
   int4* trect;          // [n] pixel rect (x0, y0, x1, y1), render.hpp:71-81
   int4* erect;          // [n] effective (alpha >= cutoff) rect, widened by 1 px
+  float4* mrow;         // [n] sub-tile mask constants (ixy/ixx, 1/ixx, q0, qcut)
   uint32_t* tcount;     // [n] overlapped tiles (0 = culled)
   double* depth;        // [n] camera-space depth (fp64)
   double2* exact;       // [n][3] fp64 (mx,my) (ixx,ixy) (iyy,op) for the guard band
@@ -31,6 +32,7 @@ struct Frame {
   // per gaussian (model order)
   DevBuf<float4> rec;
   DevBuf<int4> trect, erect;
+  DevBuf<float4> mrow;        // sub-tile mask row-interval constants
   DevBuf<uint32_t> tcount, dup_base;
   DevBuf<double> depth;
   DevBuf<double2> exact;     // [n][3] fp64 mean2d, conic, opacity
