@@ -508,6 +508,11 @@ def main():
     # real stdout for the single JSON line and send everything else to stderr.
     json_out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
+    # watchdog: a hung rank dumps every thread's stack and exits instead of
+    # holding the GPUs until the launcher's limit
+    import faulthandler
+    faulthandler.dump_traceback_later(float(os.environ.get("DSG_BENCH_WATCHDOG_S", "900")),
+                                      exit=True)
     dist = Dist()
     if args.gpus != dist.world:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {dist.world}; using WORLD_SIZE")

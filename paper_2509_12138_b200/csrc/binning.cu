@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool vis = false;
-  float depth_f = 0.f;
+  double dep = 0.0;
   if (i < a.n) {
     double p[kParams];
 #pragma unroll
@@ -80,75 +80,123 @@ __global__ void __launch_bounds__(256) k_preprocess(PreprocessArgs a) {
         ex[0] = make_double2(pr.mx, pr.my);
         ex[1] = make_double2(ixx, ixy);
         ex[2] = make_double2(iyy, op);
-        depth_f = (float)pr.depth;
+        dep = pr.depth;
         vis = true;
       }
     }
     a.tcount[i] = count;
   }
-  // warp-aggregated compaction of the visible set (order fixed by the sort)
-  uint32_t mask = __ballot_sync(0xffffffffu, vis);
-  uint32_t base = 0;
-  if (mask != 0 && lane == __ffs(mask) - 1) base = atomicAdd(a.vis_count, (uint32_t)__popc(mask));
-  base = __shfl_sync(0xffffffffu, base, mask != 0 ? __ffs(mask) - 1 : 0);
-  if (vis) {
-    uint32_t slot = base + __popc(mask & ((1u << lane) - 1u));
-    a.vis_key[slot] = __float_as_uint(depth_f);
-    a.vis_idx[slot] = (uint32_t)i;
-  }
-  // key range of the visible set: the depth sort only needs the bits of
-  // (key - min), typically 24 of 32 (3 radix passes instead of 4)
-  uint32_t kmin = vis ? __float_as_uint(depth_f) : 0xffffffffu;
-  uint32_t kmax = vis ? __float_as_uint(depth_f) : 0u;
+  // fp64 depth range of the visible set (positive doubles order like their
+  // bits): the depth keys quantise [dmin, dmax] to 32 bits (k_vis_compact)
+  unsigned long long dmin = vis ? (unsigned long long)__double_as_longlong(dep) : ~0ull;
+  unsigned long long dmax = vis ? (unsigned long long)__double_as_longlong(dep) : 0ull;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-    kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+    dmin = min(dmin, __shfl_xor_sync(0xffffffffu, dmin, o));
+    dmax = max(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
   }
   // one pair of atomics per block, and only when it can move the bound
   // (same-address atomics from every warp serialise in L2)
-  __shared__ uint32_t smin[8], smax[8];
+  __shared__ unsigned long long smin[8], smax[8];
   const int warp = threadIdx.x >> 5;
   if (lane == 0) {
-    smin[warp] = kmin;
-    smax[warp] = kmax;
+    smin[warp] = dmin;
+    smax[warp] = dmax;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-      kmin = min(kmin, smin[w]);
-      kmax = max(kmax, smax[w]);
+      dmin = min(dmin, smin[w]);
+      dmax = max(dmax, smax[w]);
     }
-    volatile uint32_t* c = a.vis_count;
-    if (kmin < c[1]) atomicMin(a.vis_count + 1, kmin);
-    if (kmax > c[2]) atomicMax(a.vis_count + 2, kmax);
+    volatile unsigned long long* c = a.drange;
+    if (dmin < c[0]) atomicMin(a.drange, dmin);
+    if (dmax > c[1]) atomicMax(a.drange + 1, dmax);
   }
 }
 
-// Re-order runs of equal fp32 depth keys by (fp64 depth, index): the
-// reference comparator (render.hpp:98-101). Runs are tiny; insertion sort.
+// Order-preserving compaction of the visible set (slot = scan of tcount != 0).
+// The key is the fp64 depth quantised over [dmin, dmax] to 32 bits: monotone
+// in the fp64 depth, and equal only for depths within range / 2^32, so the
+// (depth, index) fix-up below has (almost) nothing to do.
+__global__ void k_vis_compact(const uint32_t* __restrict__ tcount, const double* __restrict__ depth,
+                              const unsigned long long* __restrict__ drange,
+                              const uint32_t* __restrict__ slot, int64_t n,
+                              uint32_t* __restrict__ vis_key, uint32_t* __restrict__ vis_idx) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n || tcount[i] == 0) return;
+  const double lo = __longlong_as_double((long long)drange[0]);
+  const double hi = __longlong_as_double((long long)drange[1]);
+  const double scale = hi > lo ? 4294967295.0 / (hi - lo) : 0.0;
+  const double q = floor((depth[i] - lo) * scale);
+  const uint32_t s = slot[i];
+  vis_key[s] = q >= 4294967295.0 ? 0xffffffffu : (uint32_t)q;
+  vis_idx[s] = (uint32_t)i;
+}
+
+// Runs of equal keys must end in (fp64 depth, index) order, the reference
+// comparator (render.hpp:98-101). They arrive index-ordered (index-ordered
+// compaction, stable sort), so exact depth ties are already right; only
+// depths closer than the key quantum can be out of order. Pass 1 marks, at
+// its run start, every run holding an out-of-order neighbour pair (read-only
+// walk back); pass 2 insertion-sorts just those runs.
+__device__ __forceinline__ bool depth_before(uint32_t u, uint32_t v, const double* depth) {
+  const double du = depth[u], dv = depth[v];
+  return du < dv || (du == dv && u < v);
+}
+
+__global__ void k_depth_mark(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx,
+                             int64_t n, const double* __restrict__ depth,
+                             uint32_t* __restrict__ runflag) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s + 1 >= n) return;
+  const uint32_t k = key[s];
+  if (key[s + 1] != k || depth_before(idx[s], idx[s + 1], depth)) return;
+  int64_t b = s;
+  while (b > 0 && key[b - 1] == k) --b;
+  runflag[b] = 1;
+}
+
+constexpr int kFixSerial = 64;  // longer flagged runs get a radix sort (bin_frame)
+
 __global__ void k_depth_fixup(const uint32_t* __restrict__ key, uint32_t* idx, int64_t n,
-                              const double* __restrict__ depth) {
-  int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= n) return;
-  uint32_t k = key[s];
-  if (s > 0 && key[s - 1] == k) return;          // not a run start
-  if (s + 1 >= n || key[s + 1] != k) return;     // singleton
+                              const double* __restrict__ depth,
+                              const uint32_t* __restrict__ runflag, uint32_t* long_runs,
+                              uint32_t long_cap) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= n || !runflag[s]) return;
+  const uint32_t k = key[s];
   int64_t e = s + 1;
   while (e < n && key[e] == k) ++e;
+  if (e - s > kFixSerial) {  // long run (many near-coincident splats): sorted separately
+    const uint32_t slot = atomicAdd(long_runs, 1u);
+    if (slot < long_cap) {
+      long_runs[1 + 2 * slot] = (uint32_t)s;
+      long_runs[2 + 2 * slot] = (uint32_t)(e - s);
+    }
+    return;
+  }
   for (int64_t j = s + 1; j < e; ++j) {
-    uint32_t v = idx[j];
-    double dv = depth[v];
+    const uint32_t v = idx[j];
     int64_t m = j - 1;
-    while (m >= s) {
-      uint32_t u = idx[m];
-      double du = depth[u];
-      if (du < dv || (du == dv && u < v)) break;
-      idx[m + 1] = u;
+    while (m >= s && !depth_before(idx[m], v, depth)) {
+      idx[m + 1] = idx[m];
       --m;
     }
     idx[m + 1] = v;
   }
+}
+
+// Long run [s, s+len): (fp64 depth bits, index) pairs for a stable radix
+// sort by depth; the run arrives index-ordered, so ties end index-ordered.
+__global__ void k_run_keys(const uint32_t* __restrict__ idx, uint32_t s, uint32_t len,
+                           const double* __restrict__ depth, unsigned long long* keys,
+                           uint32_t* vals) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= len) return;
+  const uint32_t v = idx[s + j];
+  keys[j] = (unsigned long long)__double_as_longlong(depth[v]);
+  vals[j] = v;
 }
 
 __global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv,
@@ -272,17 +320,48 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd,
   if (e == nd - 1 || (tile_key[e + 1] & kTileIdMask) != t) ranges[t].y = (uint32_t)(e + 1);
 }
 
+// Blend work units (blend.cu): tile i of the longest-first order gets
+// ceil(len / seg_len) segments (at least one, so empty tiles still write the
+// background); units of a tile are consecutive.
+__global__ void k_unit_counts(const uint2* __restrict__ ranges, const uint32_t* __restrict__ order,
+                              int nt, uint32_t seg, uint32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const uint2 r = ranges[order[i]];
+  cnt[i] = max(1u, (r.y - r.x + seg - 1) / seg);
+}
+
+// Layout: unit i (< nt) = first segment of ordered tile i; segment k >= 1 of
+// tile i = unit nt + (base[i] - i) + k - 1 (base[i] - i = later segments of
+// earlier tiles); first_of maps a later unit back to its tile's first unit.
+__global__ void k_unit_fill(const uint2* __restrict__ ranges, const uint32_t* __restrict__ order,
+                            int nt, uint32_t seg, const uint32_t* __restrict__ base,
+                            uint4* __restrict__ units, uint32_t* __restrict__ first_of) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nt) return;
+  const uint32_t t = order[i];
+  const uint2 r = ranges[t];
+  const uint32_t b = base[i], nseg = base[i + 1] - b;
+  for (uint32_t k = 0; k < nseg; ++k) {
+    const uint32_t beg = r.x + k * seg, end = min(r.y, beg + seg);
+    const uint32_t u = k == 0 ? (uint32_t)i : (uint32_t)nt + (b - i) + k - 1;
+    units[u] = make_uint4(t, beg, end, k | (nseg << 16));
+    if (k > 0) first_of[u - nt] = (uint32_t)i;
+  }
+}
+
 // Longest-first tile schedule for the blend kernels: tiles are bucketed by
 // floor(log2(list length)) and emitted heaviest bucket first, so the long
 // lists start early instead of forming the tail (order inside a bucket is
 // irrelevant: tiles are independent).
-__global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t* bins,
-                            uint32_t* counts) {
+__global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t seg,
+                            uint32_t* bins, uint32_t* counts) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint2 r = ranges[t0 + i];
   const uint32_t len = r.y - r.x;
-  const uint32_t b = len ? 32u - __clz(len) : 0u;  // 0..32
+  // bin 33 = multi-segment lists (len > seg): they lead the order
+  const uint32_t b = len > seg ? 33u : (len ? 32u - __clz(len) : 0u);
   bins[i] = b;
   atomicAdd(&counts[b], 1u);
 }
@@ -290,7 +369,7 @@ __global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, ui
 __global__ void k_tile_bin_offsets(uint32_t* counts) {  // one warp: descending exclusive scan
   const int lane = threadIdx.x;
   uint32_t run = 0;
-  for (int b = 32; b >= 0; --b) {
+  for (int b = 33; b >= 0; --b) {
     const uint32_t c = counts[b];
     if (lane == 0) counts[b] = run;
     run += c;
@@ -321,6 +400,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.trect.ensure(std::max<int64_t>(n, 1));
   f.erect.ensure(std::max<int64_t>(n, 1));
   f.mrow.ensure(std::max<int64_t>(n, 1));
+  f.vslot.ensure(n + 1);
   f.tcount.ensure(std::max<int64_t>(n, 1));
   f.depth.ensure(std::max<int64_t>(n, 1));
   f.exact.ensure(3 * (size_t)std::max<int64_t>(n, 1));
@@ -331,9 +411,9 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.vis_idx2.ensure(std::max<int64_t>(n, 1));
   f.offs.ensure(std::max<int64_t>(n, 1) + 1);
   f.ranges.ensure(f.tiles);
-  f.counters.ensure(4);
-  DSG_CUDA_CHECK(cudaMemsetAsync(f.counters.get(), 0, 4 * sizeof(uint32_t), st));
-  DSG_CUDA_CHECK(cudaMemsetAsync(f.counters.get() + 1, 0xff, sizeof(uint32_t), st));  // key min
+  f.drange.ensure(2);
+  DSG_CUDA_CHECK(cudaMemsetAsync(f.drange.get(), 0xff, sizeof(unsigned long long), st));  // min
+  DSG_CUDA_CHECK(cudaMemsetAsync(f.drange.get() + 1, 0, sizeof(unsigned long long), st));  // max
   DSG_CUDA_CHECK(cudaMemsetAsync(f.ranges.get(), 0, f.tiles * sizeof(uint2), st));
   f.n_visible = 0;
   f.n_dup = 0;
@@ -351,32 +431,39 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     a.tcount = f.tcount.get();
     a.depth = f.depth.get();
     a.exact = f.exact.get();
-    a.vis_key = f.vis_key.get();
-    a.vis_idx = f.vis_idx.get();
-    a.vis_count = f.counters.get();
+    a.drange = f.drange.get();
     k_preprocess<<<blocks(n, 256), 256, 0, st>>>(a);
     count_launch();
     DSG_CUDA_CHECK(cudaGetLastError());
+    exclusive_scan_u32(f.tcount.get(), f.vslot.get(), n, f.scan, st, true);
+    k_vis_compact<<<blocks(n, 256), 256, 0, st>>>(f.tcount.get(), f.depth.get(), f.drange.get(),
+                                                  f.vslot.get(), n, f.vis_key.get(),
+                                                  f.vis_idx.get());
+    count_launch();
     tm.mark(1, st);
-    uint32_t c3[3] = {0, 0, 0};
-    DSG_CUDA_CHECK(cudaMemcpyAsync(c3, f.counters.get(), 3 * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    uint32_t nvis = 0;
+    DSG_CUDA_CHECK(cudaMemcpyAsync(&nvis, f.vslot.get() + n, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                                   st));
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-    f.n_visible = c3[0];
-    f.key_min = c3[1];
-    f.key_max = c3[2];
+    f.n_visible = nvis;
   }
   const int64_t nv = f.n_visible;
   if (nv == 0) return;
-  int depth_bits = 1;
-  while (depth_bits < 32 && ((uint64_t)(f.key_max - f.key_min) >> depth_bits) != 0) ++depth_bits;
+
   // depth sort of the visible set (stable; key = fp32 depth bits)
   bool alt = radix_sort_pairs<uint32_t>(f.vis_key.get(), f.vis_idx.get(), f.vis_key2.get(),
-                                         f.vis_idx2.get(), nv, 0, depth_bits, f.sort, st,
-                                         f.key_min, false);
+                                         f.vis_idx2.get(), nv, 0, 32, f.sort, st, 0u, false);
   uint32_t* skey = alt ? f.vis_key2.get() : f.vis_key.get();
   uint32_t* sidx = alt ? f.vis_idx2.get() : f.vis_idx.get();
-  k_depth_fixup<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get());
-  count_launch();
+  uint32_t* runflag = alt ? f.vis_key.get() : f.vis_key2.get();  // free until k_gather_counts
+  DSG_CUDA_CHECK(cudaMemsetAsync(runflag, 0, sizeof(uint32_t) * nv, st));
+  constexpr uint32_t kLongCap = 1024;
+  uint32_t* long_runs = f.long_runs.ensure(1 + 2 * kLongCap);
+  DSG_CUDA_CHECK(cudaMemsetAsync(long_runs, 0, sizeof(uint32_t), st));
+  k_depth_mark<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get(), runflag);
+  k_depth_fixup<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get(), runflag,
+                                                 long_runs, kLongCap);
+  count_launch(2);
   tm.mark(2, st);
   f.sorted_idx = sidx;
   // per-splat tile counts in depth order, exclusive scan -> duplicate slots
@@ -384,9 +471,34 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
   count_launch();
   exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
-  uint32_t nd = 0;
+  uint32_t nd = 0, n_long = 0;
   DSG_CUDA_CHECK(cudaMemcpyAsync(&nd, f.offs.get() + nv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaMemcpyAsync(&n_long, long_runs, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (n_long > 0) {
+    // rare: long runs of near-coincident depths with out-of-order pairs.
+    // Radix-sort each by its fp64 depth bits, then redo the slots (the
+    // duplicate total is order-independent).
+    if (n_long > kLongCap) fail(kInvalidArgument, "too many long equal-depth runs");
+    std::vector<uint32_t> runs(2 * n_long);
+    DSG_CUDA_CHECK(cudaMemcpy(runs.data(), long_runs + 1, sizeof(uint32_t) * 2 * n_long,
+                              cudaMemcpyDeviceToHost));
+    for (uint32_t r = 0; r < n_long; ++r) {
+      const uint32_t s0 = runs[2 * r], len = runs[2 * r + 1];
+      unsigned long long* rk = f.run_keys.ensure(2 * (size_t)len);
+      uint32_t* rv = f.run_vals.ensure(2 * (size_t)len);
+      k_run_keys<<<blocks(len, 256), 256, 0, st>>>(sidx, s0, len, f.depth.get(), rk, rv);
+      count_launch();
+      const bool in_alt = radix_sort_pairs<uint64_t>(
+          reinterpret_cast<uint64_t*>(rk), rv, reinterpret_cast<uint64_t*>(rk) + len, rv + len, len,
+          0, 64, f.sort, st);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(sidx + s0, in_alt ? rv + len : rv, sizeof(uint32_t) * len,
+                                     cudaMemcpyDeviceToDevice, st));
+    }
+    k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+    count_launch();
+    exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
+  }
   f.n_dup = nd;
   f.tile_key.ensure(std::max<uint32_t>(nd, 1));
   f.dup_val.ensure(std::max<uint32_t>(nd, 1));
@@ -416,14 +528,33 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     const int t0 = cam.band_ty0 * cam.tiles_x;
     const int nt = (cam.band_ty1 - cam.band_ty0) * cam.tiles_x;
     f.tile_order.ensure(std::max(nt, 1));
-    f.tile_bins.ensure(std::max(nt, 1) + 33);
+    f.tile_bins.ensure(std::max(nt, 1) + 34);
     uint32_t* counts = f.tile_bins.get() + std::max(nt, 1);
-    DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, 33 * sizeof(uint32_t), st));
-    k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, f.tile_bins.get(), counts);
+    DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, 34 * sizeof(uint32_t), st));
+    f.seg_len = std::max<int64_t>(kSegMin, ((int64_t)nd + kSegDiv - 1) / kSegDiv);
+    f.seg_len = (f.seg_len + 31) & ~int64_t(31);  // whole 32-entry chunks
+    k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, (uint32_t)f.seg_len,
+                                                 f.tile_bins.get(), counts);
     k_tile_bin_offsets<<<1, 32, 0, st>>>(counts);
     k_tile_order<<<blocks(nt, 256), 256, 0, st>>>(f.tile_bins.get(), t0, nt, counts,
                                                   f.tile_order.get());
     count_launch(3);
+    // blend work units: ceil(len / seg_len) per tile in that order
+    f.band_tiles = nt;
+    f.unit_cap = nt + (int64_t)nd / f.seg_len + 1;
+    f.units.ensure(f.unit_cap);
+    f.unit_base.ensure(nt + 1);
+    f.nonlast.ensure(std::max<int64_t>(f.unit_cap - nt, 1));
+    f.ubuf.ensure((size_t)kUnitPlanes * f.unit_cap * kTile * kTile);
+    uint32_t* ucnt = f.tile_bins.get();  // bins are consumed by k_tile_order
+    k_unit_counts<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), f.tile_order.get(), nt,
+                                                   (uint32_t)f.seg_len, ucnt);
+    count_launch();
+    exclusive_scan_u32(ucnt, f.unit_base.get(), nt, f.scan, st);
+    k_unit_fill<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), f.tile_order.get(), nt,
+                                                 (uint32_t)f.seg_len, f.unit_base.get(),
+                                                 f.units.get(), f.nonlast.get());
+    count_launch();
   }
   DSG_CUDA_CHECK(cudaGetLastError());
   tm.mark(4, st);

@@ -84,7 +84,8 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
                       bool skip_trivial = true);
 
 // Exclusive prefix sum of n u32 into out (out[n] = total). out may alias in.
+// flags: sum (in[i] != 0) instead of in[i] (order-preserving compaction).
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratch& s,
-                        cudaStream_t st);
+                        cudaStream_t st, bool flags = false);
 
 }  // namespace dsg

@@ -6,6 +6,16 @@
 
 namespace dsg {
 
+// Blend work units split a tile list only when it is long enough to form
+// the kernel's tail: segment length = max(kSegMin, n_dup / kSegDiv), i.e. a
+// list longer than the average work of ~kSegDiv/8 concurrent warps.
+#ifndef DSG_SEG_MIN
+#define DSG_SEG_MIN 2048
+#endif
+constexpr int kSegMin = DSG_SEG_MIN;
+constexpr int kSegDiv = 128;
+constexpr int kUnitPlanes = 7;  // per-unit per-pixel planes (blend.cu UnitPlane)
+
 struct PreprocessArgs {
   const float* params;  // [14][pitch] planar fp32 model
   int64_t pitch, n;
@@ -18,16 +28,13 @@ struct PreprocessArgs {
   uint32_t* tcount;     // [n] overlapped tiles (0 = culled)
   double* depth;        // [n] camera-space depth (fp64)
   double2* exact;       // [n][3] fp64 (mx,my) (ixx,ixy) (iyy,op) for the guard band
-  uint32_t* vis_key;    // [n] compacted fp32 depth bits
-  uint32_t* vis_idx;    // [n] compacted gaussian index
-  uint32_t* vis_count;
+  unsigned long long* drange;  // [2] fp64 depth min / max bits of the visible set
 };
 
 // Scratch for one rendered view: binning products, per-pixel forward state,
 // loss buffers and backward partials.
 struct Frame {
   int64_t n = 0, n_visible = 0, n_dup = 0, tiles = 0;
-  uint32_t key_min = 0, key_max = 0;  // fp32 depth-key range of the visible set
   int width = 0, height = 0;
   // per gaussian (model order)
   DevBuf<float4> rec;
@@ -38,6 +45,10 @@ struct Frame {
   DevBuf<double2> exact;     // [n][3] fp64 mean2d, conic, opacity
   // visible set, depth-sorted
   DevBuf<uint32_t> vis_key, vis_idx, vis_key2, vis_idx2, offs;
+  DevBuf<uint32_t> vslot;        // visible-slot scan (order-preserving compaction)
+  DevBuf<unsigned long long> drange;
+  DevBuf<uint32_t> long_runs, run_vals;  // long equal-key runs needing a radix sort
+  DevBuf<unsigned long long> run_keys;
   uint32_t* sorted_idx = nullptr;
   // duplicates
   DevBuf<uint32_t> tile_key, dup_val, tile_key2, dup_val2;
@@ -46,6 +57,22 @@ struct Frame {
   DevBuf<uint2> ranges;
   DevBuf<uint8_t> emask;      // per sorted entry: touched 8x4 sub-tiles of its tile
   DevBuf<uint32_t> tile_order, tile_bins;  // longest-first blend schedule (band tiles)
+  // blend work units: (tile, <= seg_len entries), tiles in longest-first order
+  DevBuf<uint4> units;
+  DevBuf<uint32_t> unit_base;  // [band tiles + 1] first unit of each ordered tile; [nt] = total
+  DevBuf<uint32_t> nonlast;    // units that are not their tile's last segment
+  DevBuf<float> ubuf;          // per unit, per pixel segment state (blend.cu UnitPlane)
+  int64_t unit_cap = 0, band_tiles = 0, seg_len = kSegMin;
+  cudaStream_t aux = nullptr;  // multi-segment forward runs beside the rest
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  Frame() = default;
+  Frame(const Frame&) = delete;
+  Frame& operator=(const Frame&) = delete;
+  ~Frame() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (aux) cudaStreamDestroy(aux);
+  }
   DevBuf<uint32_t> counters;
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL;

@@ -226,14 +226,15 @@ constexpr int kScanItems = 8;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in,
-                                                              int64_t n, uint32_t* sums) {
+                                                              int64_t n, uint32_t* sums,
+                                                              bool flags) {
   __shared__ uint32_t tmp[32];
   int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
     int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
-    if (idx < n) s += in[idx];
+    if (idx < n) s += flags ? (uint32_t)(in[idx] != 0) : in[idx];
   }
   uint32_t agg;
   block_exclusive_sum<kScanThreads>(s, &agg, tmp);
@@ -260,14 +261,15 @@ __global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, int64_t nb) 
 
 __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __restrict__ in,
                                                             uint32_t* out, int64_t n,
-                                                            const uint32_t* __restrict__ sums) {
+                                                            const uint32_t* __restrict__ sums,
+                                                            bool flags) {
   __shared__ uint32_t tmp[32];
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
   uint32_t local = 0;
 #pragma unroll
   for (int i = 0; i < kScanItems; ++i) {
-    v[i] = (base + i < n) ? in[base + i] : 0u;
+    v[i] = (base + i < n) ? (flags ? (uint32_t)(in[base + i] != 0) : in[base + i]) : 0u;
     local += v[i];
   }
   uint32_t agg;
@@ -288,18 +290,18 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __re
 }  // namespace
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratch& s,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool flags) {
   if (n <= 0) {
     DSG_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(uint32_t), st));
     return;
   }
   int64_t nb = (n + kScanTile - 1) / kScanTile;
   uint32_t* sums = s.block_sums.ensure(nb + 1);
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums);
+  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums, flags);
   count_launch();
   k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
   count_launch();
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums);
+  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums, flags);
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }

@@ -196,3 +196,29 @@ def test_exact_submasks_change_nothing(ctx, scene):
     for a, b in zip(*outs):
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("cluster", [40, 3000])
+def test_near_coincident_depth_order(orc, ctx, cluster):
+    """Many splats at (nearly) the same depth: exact ties, and depths closer
+    than the 32-bit key quantum in shuffled index order. The order must still
+    be the reference's (fp64 depth, index) order — short runs are fixed in
+    place, long ones by a radix sort on the fp64 depth bits."""
+    rng = np.random.default_rng(cluster)
+    model = fp32_exact(random_scene(17, cluster + 500))
+    c = model.params[:cluster].copy()
+    c[:, 0:3] = [0.05, -0.03, 0.1]
+    # every other splat nudged by one fp32 ulp in z: depth differences far
+    # below the key quantum, in index order opposite to depth order
+    nudge = rng.integers(0, 3, cluster).astype(np.float64)
+    c[:, 2] = np.float32(0.1) + nudge * np.spacing(np.float32(0.1))
+    model.params[:cluster] = c
+    # one distant splat widens the depth range so the key quantum (range /
+    # 2^32) exceeds the nudges: the whole cluster shares one key
+    model.params[cluster, 0:3] = [0.0, 0.0, 40.0]
+    model = fp32_exact(model)
+    cam = make_camera(96)
+    a = api.render(model, cam, RenderConfig(), ctx=ctx)
+    b = orc.render(model, cam, RenderConfig())
+    np.testing.assert_array_equal(a.splat_order, b.splat_order)
+    assert np.max(np.abs(a.color - b.color)) <= 1e-3
