@@ -13,7 +13,10 @@ namespace dsg {
 #define DSG_SEG_MIN 2048
 #endif
 constexpr int kSegMin = DSG_SEG_MIN;
-constexpr int kSegDiv = 128;
+#ifndef DSG_SEG_DIV
+#define DSG_SEG_DIV 512
+#endif
+constexpr int kSegDiv = DSG_SEG_DIV;
 constexpr int kUnitPlanes = 7;  // per-unit per-pixel planes (blend.cu UnitPlane)
 
 struct PreprocessArgs {
@@ -63,16 +66,6 @@ struct Frame {
   DevBuf<uint32_t> nonlast;    // units that are not their tile's last segment
   DevBuf<float> ubuf;          // per unit, per pixel segment state (blend.cu UnitPlane)
   int64_t unit_cap = 0, band_tiles = 0, seg_len = kSegMin;
-  cudaStream_t aux = nullptr;  // multi-segment forward runs beside the rest
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  Frame() = default;
-  Frame(const Frame&) = delete;
-  Frame& operator=(const Frame&) = delete;
-  ~Frame() {
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (aux) cudaStreamDestroy(aux);
-  }
   DevBuf<uint32_t> counters;
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL;
