@@ -251,8 +251,8 @@ def algorithmic_bytes(stage: str, n: int, nv: int, npix: int, n_dup: int) -> flo
     """Minimal HBM bytes one launch must move."""
     return {
         "preprocess": 56.0 * n + 4.0 * n + 104.0 * nv,     # params in; count; payload+rect+depth+key out
-        "depth_sort": 3 * 16.0 * nv + 8.0 * nv,            # 3 passes (24-bit key range) x (key,val) r+w + histogram read
-        "scan_duplicate": 12.0 * nv + 12.0 * n_dup,        # counts, scan, (tile,val) pairs out
+        "depth_sort": 4 * 16.0 * nv + 8.0 * nv,            # 4 passes (32-bit key) x (key,val) r+w + histogram read
+        "scan_duplicate": 64.0 * nv + 8.0 * n_dup,         # counts, scan, rects + mask constants in, (tile|mask, idx) out
         "tile_sort_ranges": 2 * 16.0 * n_dup + 9.0 * n_dup,  # 2 passes, ranges + sub-tile masks
         "blend_fwd": 5.0 * n_dup + 48.0 * n_dup + 20.0 * npix,   # list + payload per entry, pixel out
         "loss": 37.0 * npix,
@@ -297,6 +297,82 @@ def load_peak():
             return float(json.load(f)["hbm_gbs"]), "measured"
     except Exception:
         return FALLBACK_HBM, "fallback"
+
+
+def run_partitioned(args, dist: Dist):
+    """BASELINE configs[2]/[3] shape: a fixed cloud cut into P partitions
+    (P >= GPUs), partition k trained on GPU k mod N (runtime.hpp:337-343
+    worker assignment). One step = one iteration of one partition; value =
+    all partitions' iterations / the slowest rank's device time."""
+    ctx = api.Context(dist.local)
+    P = args.partitions
+    n_total = args.n_total or scenes.SIZES[args.workload]
+    t0 = time.time()
+    pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    parts = api.partition_cloud(pts, P, 3.0 * nn, ctx=ctx)
+    rig = scenes.rig_for_cloud(pts, args.az, args.el, args.res)
+    train_idx, _ = split_rig(len(rig), 0.1, 1)
+    cams = [rig[i] for i in train_idx]
+    rcfg = RenderConfig()
+    mine = [k for k in range(P) if k % dist.world == dist.rank]
+    work = []
+    for k in mine:
+        part = parts[k]
+        idx = np.concatenate([part.owned_indices, part.ghost_indices]).astype(np.int64)
+        ppts, pcols = np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx])
+        gt = api.ground_truth_model(ppts, pcols, nn, 0.97, ctx=ctx)
+        views = api.DeviceViews.synthesize(ctx, gt, rcfg, cams, ppts, True, 2.0, 2.0)
+        del gt
+        seeds = api.seed_gaussians(ppts, pcols, 3, ctx=ctx)
+        work.append((k, seeds, seeds.download(), views))
+    log(f"[rank {dist.rank}] partitions {mine} of {P}: cloud {n_total:,} pts, sizes "
+        f"{[len(w[2]) for w in work]}, {len(cams)} views at {args.res}^2, setup {time.time() - t0:.1f}s")
+    for k, dm, host, views in work:  # warm-up
+        if args.warmup > 0:
+            api.train_device(dm, views, TrainConfig(iterations=args.warmup, seed=1 + k))
+            dm.upload(host)
+    ctx.synchronize()
+    clocks = ClockSampler(dist.local)
+    clocks.start()
+    dist.barrier()
+    ctx.synchronize()
+    dev_ms, launches0 = 0.0, api.launch_count()
+    with api.nvtx_range("dsg_timed"):
+        for k, dm, host, views in work:
+            api.train_device(dm, views, TrainConfig(iterations=args.steps, seed=1 + k))
+            dev_ms += ctx.last_timing()[0]
+        ctx.synchronize()
+    launches = api.launch_count() - launches0
+    dist.barrier()
+    clk = clocks.stop()
+    t_max = dist.max(dev_ms) / 1e3
+    n_local = float(sum(len(w[2]) for w in work))
+    total_iters = P * args.steps
+    gv = dist.sum(n_local * args.steps) / t_max
+    return {
+        "metric": METRIC,
+        "value": round(total_iters / t_max, 3),
+        "unit": "it/s",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(t_max * 1e3 / (args.steps * len(work)), 4),
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f32 (fp64 for ordering/cutoff decisions, SSIM statistics and the 3D chain)",
+        "data": "synthetic",
+        "config": {"workload": f"{args.workload}-shaped isosurface, {n_total:,} Gaussians in {P} slab "
+                               f"partitions (+ghosts), partition k on GPU k mod {dist.world}, "
+                               f"{args.az}x{args.el} rig at {args.res}^2",
+                   "partitions": P, "gaussians": n_total, "resolution": args.res,
+                   "views": len(cams), "l2": "working set > L2"},
+        "gaussian_views_per_sec": round(gv, 1),
+        "e2e": None,
+        "gpu_launches": int(dist.sum(float(launches))),
+        "clocks": clk,
+    }
 
 
 def run_ours(args, dist: Dist):
@@ -501,6 +577,9 @@ def main():
     ap.add_argument("--el", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-global", action="store_true", help="skip the merge + 4K render phase")
+    ap.add_argument("--partitions", type=int, default=0,
+                    help="P > GPUs: fixed cloud in P partitions, k on GPU k mod N (configs 3/4)")
+    ap.add_argument("--n-total", type=int, default=None, help="cloud size for --partitions")
     args = ap.parse_args()
     if args.n_per_gpu is None:
         args.n_per_gpu = scenes.SIZES[args.workload]
@@ -518,6 +597,8 @@ def main():
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {dist.world}; using WORLD_SIZE")
     if args.impl == "reference":
         line = run_reference(args, dist)
+    elif args.partitions and args.partitions != dist.world:
+        line = run_partitioned(args, dist)
     else:
         line = run_ours(args, dist)
     if dist.rank == 0 and line is not None:

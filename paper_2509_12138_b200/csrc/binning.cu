@@ -452,7 +452,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
 
   // depth sort of the visible set (stable; key = fp32 depth bits)
   bool alt = radix_sort_pairs<uint32_t>(f.vis_key.get(), f.vis_idx.get(), f.vis_key2.get(),
-                                         f.vis_idx2.get(), nv, 0, 32, f.sort, st, 0u, false);
+                                         f.vis_idx2.get(), nv, 0, 32, f.sort, st, false);
   uint32_t* skey = alt ? f.vis_key2.get() : f.vis_key.get();
   uint32_t* sidx = alt ? f.vis_idx2.get() : f.vis_idx.get();
   uint32_t* runflag = alt ? f.vis_key.get() : f.vis_key2.get();  // free until k_gather_counts
@@ -516,8 +516,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   int tile_bits = 1;
   while ((int64_t(1) << tile_bits) < f.tiles) ++tile_bits;
   bool alt2 = radix_sort_pairs<uint32_t>(f.tile_key.get(), f.dup_val.get(), f.tile_key2.get(),
-                                          f.dup_val2.get(), nd, 0, tile_bits, f.sort, st, 0u,
-                                          false);
+                                          f.dup_val2.get(), nd, 0, tile_bits, f.sort, st, false);
   f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
   f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
   f.emask.ensure(std::max<uint32_t>(nd, 1));

@@ -74,13 +74,11 @@ struct ScanScratch {
 // (keys, vals) and (keys_alt, vals_alt); returns true when the sorted result
 // ends in the *_alt buffers. Digits whose histogram is a single bin are
 // skipped (stable no-op). Synchronizes the stream once (histogram readback).
-// Digits are taken from (key - offset), so a key range known to start at
-// `offset` needs only end_bit = bit-length(max - offset) bits. With
-// skip_trivial = false every pass runs and the call never synchronizes
+// With skip_trivial = false every pass runs and the call never synchronizes
 // (the per-step sorts, whose digits all vary).
 template <class K>
 bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
-                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset = 0,
+                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st,
                       bool skip_trivial = true);
 
 // Exclusive prefix sum of n u32 into out (out[n] = total). out may alias in.

@@ -44,7 +44,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 template <class K>
 __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, int64_t n,
-                                                    int begin_bit, int passes, K offset,
+                                                    int begin_bit, int passes,
                                                     uint32_t* __restrict__ ghist) {
   // 4 copies (one per warp pair) of up to 8 passes x 256 bins. Each thread
   // counts runs of equal digits in registers and flushes a run with one
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
   }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const K k = keys[i] - offset;
+    const K k = keys[i];
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       if (p >= passes) break;
@@ -110,9 +110,12 @@ struct OnesweepSmem {
 };
 
 template <class K>
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(
+#ifndef DSG_SORT_MINB
+#define DSG_SORT_MINB 2  // 2 CTAs/SM: 128 registers, no spills (unbounded: 155, 1 CTA/SM)
+#endif
+__global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
-    uint32_t* __restrict__ vout, int64_t n, int shift, K offset,
+    uint32_t* __restrict__ vout, int64_t n, int shift,
     const uint32_t* __restrict__ gscan, uint32_t* status, uint32_t* counter) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem<K>& sm = *reinterpret_cast<OnesweepSmem<K>*>(smem_raw);
@@ -134,7 +137,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
     bool valid = idx < n;
     k[i] = valid ? kin[idx] : K(0);
     v[i] = valid ? vin[idx] : 0u;
-    dig[i] = valid ? (uint32_t)(((K)(k[i] - offset) >> shift) & (kRadix - 1)) : 0x100u;
+    dig[i] = valid ? (uint32_t)((k[i] >> shift) & (kRadix - 1)) : 0x100u;
   }
   const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(
   const int count = remain < kPart ? (int)remain : kPart;
   for (int j = tid; j < count; j += kSortThreads) {
     K key = sm.keys[j];
-    uint32_t dg = (uint32_t)(((K)(key - offset) >> shift) & (kRadix - 1));
+    uint32_t dg = (uint32_t)((key >> shift) & (kRadix - 1));
     uint32_t out = sm.global_base[dg] + (uint32_t)j - sm.block_excl[dg];
     kout[out] = key;
     vout[out] = sm.vals[j];
@@ -308,7 +311,7 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratc
 
 template <class K>
 bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, int64_t n,
-                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st, K offset,
+                      int begin_bit, int end_bit, SortScratch& s, cudaStream_t st,
                       bool skip_trivial) {
   if (n <= 1 || end_bit <= begin_bit) return false;
   if (n > (int64_t)kValueMask) fail(kInvalidArgument, "radix sort: too many keys");
@@ -321,7 +324,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
   DSG_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * passes * parts * kRadix, st));
   DSG_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * passes, st));
   int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, offset, hist);
+  k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, hist);
   count_launch();
   // Which digits actually vary? (a single populated bin = identity pass)
   std::vector<bool> trivial(passes, false);
@@ -347,7 +350,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
     K* ko = in_alt ? keys : keys_alt;
     uint32_t* vo = in_alt ? vals : vals_alt;
     k_onesweep<K><<<(unsigned)parts, kSortThreads, smem, st>>>(
-        ki, vi, ko, vo, n, begin_bit + kRadixBits * p, offset, hist + (size_t)p * kRadix,
+        ki, vi, ko, vo, n, begin_bit + kRadixBits * p, hist + (size_t)p * kRadix,
         status + (size_t)p * parts * kRadix, counters + p);
     count_launch();
     in_alt = !in_alt;
@@ -357,8 +360,8 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
 }
 
 template bool radix_sort_pairs<uint32_t>(uint32_t*, uint32_t*, uint32_t*, uint32_t*, int64_t, int,
-                                         int, SortScratch&, cudaStream_t, uint32_t, bool);
+                                         int, SortScratch&, cudaStream_t, bool);
 template bool radix_sort_pairs<uint64_t>(uint64_t*, uint32_t*, uint64_t*, uint32_t*, int64_t, int,
-                                         int, SortScratch&, cudaStream_t, uint64_t, bool);
+                                         int, SortScratch&, cudaStream_t, bool);
 
 }  // namespace dsg
