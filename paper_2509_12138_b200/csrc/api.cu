@@ -276,6 +276,7 @@ void backward_dev(dsg_ctx ctx, ModelDev& m, const CamDev& cam, const RenderDev& 
   a.tcount = f.tcount.get();
   a.dup_base = f.dup_base.get();
   a.partials = f.partials.get();
+  a.n_dup = f.n_dup;
   a.tmask = f.tmask.get();
   a.grads = m.grads.get();
   a.dmean = m.dmean.get();
@@ -946,6 +947,7 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
         a.tcount = f.tcount.get();
         a.dup_base = f.dup_base.get();
         a.partials = f.partials.get();
+        a.n_dup = f.n_dup;
         a.tmask = f.tmask.get();
         a.grads = m.grads.get();
         a.dmean = m.dmean.get();

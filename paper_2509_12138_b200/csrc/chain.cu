@@ -63,13 +63,21 @@ __global__ void __launch_bounds__(256) k_chain(ChainArgs a) {
       uint32_t m = (a.tmask[d >> 2] >> (8 * (d & 3))) & 0xffu;
       if (!m) continue;
       touched = true;
-      const float* pp = a.partials + (size_t)d * 8 * 9;
+      const float4* pp = reinterpret_cast<const float4*>(a.partials) + (size_t)d * 8 * 2;
+      const float* p8 = a.partials + (size_t)a.n_dup * 64 + (size_t)d * 8;
       while (m) {
         const int w = __ffs(m) - 1;
         m &= m - 1;
-        const float* q = pp + w * 9;
-#pragma unroll
-        for (int v = 0; v < 9; ++v) acc[v] += q[v];
+        const float4 q0 = pp[2 * w], q1 = pp[2 * w + 1];
+        acc[0] += q0.x;
+        acc[1] += q0.y;
+        acc[2] += q0.z;
+        acc[3] += q0.w;
+        acc[4] += q1.x;
+        acc[5] += q1.y;
+        acc[6] += q1.z;
+        acc[7] += q1.w;
+        acc[8] += p8[w];
       }
     }
   }

@@ -71,8 +71,8 @@ struct Frame {
   DevBuf<float> rgb, T, dL;
   DevBuf<uint32_t> last;
   DevBuf<int32_t> ncontrib;
-  // backward partials [n_dup][10]
-  DevBuf<float> partials;     // [n_dup][8 sub-tiles][9] screen gradients
+  // backward partials: [n_dup][8 sub-tiles][8] (values 0..7) then [n_dup][8] (value 8)
+  DevBuf<float> partials;
   DevBuf<uint32_t> tmask;     // 8-bit touched-sub-tile mask per duplicate, 4 per word
   // device copy of the blend kernels' guard-band context (read by the rare
   // fp64 path through a pointer, so it never lands on the thread stack)
@@ -102,7 +102,8 @@ struct ChainArgs {
   CamDev cam;
   const uint32_t* tcount;
   const uint32_t* dup_base;
-  const float* partials;
+  const float* partials;    // blend.cu layout: [n_dup][8][8] then [n_dup][8]
+  int64_t n_dup;
   const uint32_t* tmask;
   float* grads;     // [14][pitch]
   float* dmean;     // [2][pitch]
