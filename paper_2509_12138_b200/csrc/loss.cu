@@ -80,6 +80,15 @@ __global__ void __launch_bounds__(kB* kB) k_ssim_stats(LossArgs a) {
     if (nc) atomicAdd(&a.counts[1], nc);
   }
   double ssum = 0.0;
+  if (nc == 0) {  // no valid masked centre in this block: P = Q = R = 0
+    if (in_img) {
+      const int64_t o = (int64_t)cy * a.w + cx;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) a.pqr[k * a.npix + o] = 0.0;
+    }
+    if (threadIdx.x == 0) a.parts[blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
+    return;
+  }
   for (int ch = 0; ch < 3; ++ch) {
     const float* X = a.x + ch * a.npix;
     const float* Y = a.y + ch * a.npix;
@@ -158,6 +167,15 @@ __global__ void __launch_bounds__(kB* kB) k_loss_grad(LossArgs a) {
   const int64_t o = (int64_t)py * a.w + px;
   const bool min = in_img && a.m[o] != 0;
   const uint32_t n_masked = a.counts[0], n_centres = a.counts[1];
+  // dL is zero off the mask: a block without a masked pixel has nothing to do
+  if (__syncthreads_count(min) == 0) {
+    if (in_img) {
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) a.dL[ch * a.npix + o] = 0.f;
+    }
+    if (threadIdx.x == 0) a.parts[a.nblocks + blockIdx.y * gridDim.x + blockIdx.x] = 0.0;
+    return;
+  }
   const bool use_ssim = a.lambda > 0.0 && n_centres > 0;
   const double l1w = n_masked ? (1.0 - a.lambda) / ((double)n_masked * 3.0) : 0.0;
   const double coeff = use_ssim ? -a.lambda / ((double)n_centres * 3.0) : 0.0;
