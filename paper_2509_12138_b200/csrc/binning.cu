@@ -118,6 +118,15 @@ __global__ void __launch_bounds__(256, DSG_PRE_MINB) k_preprocess(PreprocessArgs
   }
 }
 
+// Depth key width (radix passes = bits / 8). Runs of equal keys (depths
+// within range / 2^bits) are put in (depth, index) order by the fix-up below;
+// 24 bits saves a pass at N=1 but makes long near-coincident runs (and their
+// radix-sort fallback) far more frequent in sparse partition views.
+#ifndef DSG_DEPTH_KEY_BITS
+#define DSG_DEPTH_KEY_BITS 32
+#endif
+constexpr int kDepthKeyBits = DSG_DEPTH_KEY_BITS;
+
 // Order-preserving compaction of the visible set (slot = scan of tcount != 0).
 // The key is the fp64 depth quantised over [dmin, dmax] to 32 bits: monotone
 // in the fp64 depth, and equal only for depths within range / 2^32, so the
@@ -130,10 +139,11 @@ __global__ void k_vis_compact(const uint32_t* __restrict__ tcount, const double*
   if (i >= n || tcount[i] == 0) return;
   const double lo = __longlong_as_double((long long)drange[0]);
   const double hi = __longlong_as_double((long long)drange[1]);
-  const double scale = hi > lo ? 4294967295.0 / (hi - lo) : 0.0;
+  const double kmax = (double)((1u << kDepthKeyBits) - 1u);
+  const double scale = hi > lo ? kmax / (hi - lo) : 0.0;
   const double q = floor((depth[i] - lo) * scale);
   const uint32_t s = slot[i];
-  vis_key[s] = q >= 4294967295.0 ? 0xffffffffu : (uint32_t)q;
+  vis_key[s] = q >= kmax ? (uint32_t)kmax : (uint32_t)q;
   vis_idx[s] = (uint32_t)i;
 }
 
@@ -455,7 +465,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
 
   // depth sort of the visible set (stable; key = fp32 depth bits)
   bool alt = radix_sort_pairs<uint32_t>(f.vis_key.get(), f.vis_idx.get(), f.vis_key2.get(),
-                                         f.vis_idx2.get(), nv, 0, 32, f.sort, st, false);
+                                         f.vis_idx2.get(), nv, 0, kDepthKeyBits, f.sort, st, false);
   uint32_t* skey = alt ? f.vis_key2.get() : f.vis_key.get();
   uint32_t* sidx = alt ? f.vis_idx2.get() : f.vis_idx.get();
   uint32_t* runflag = alt ? f.vis_key.get() : f.vis_key2.get();  // free until k_gather_counts
