@@ -452,8 +452,9 @@ def run_ours(args, dist: Dist):
                "download_s": round(e0 + e_wall - e2, 4)}
     e_max = dist.max(e_wall)
     view_bytes = npix * (3 * 4 + 1)
-    h2d = view_bytes + n * 14 * 8 / args.steps
-    d2h = 8 + n * 14 * 8 / args.steps
+    # the model crosses the bus as fp32 (host converts from/to doubles)
+    h2d = view_bytes + n * 14 * 4 / args.steps
+    d2h = 8 + n * 14 * 4 / args.steps
     del out
 
     peak, peak_kind = load_peak()

@@ -200,18 +200,20 @@ RenderDev make_rd(const dsg_render_config* c) {
 }
 
 // ---- layout conversion kernels -------------------------------------------------
-__global__ void k_aos_to_planar(const double* __restrict__ aos, int64_t n, int C,
+template <class A>
+__global__ void k_aos_to_planar(const A* __restrict__ aos, int64_t n, int C,
                                 float* __restrict__ planar, int64_t pitch) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   for (int c = 0; c < C; ++c) planar[c * pitch + i] = (float)aos[i * C + c];
 }
 
+template <class A>
 __global__ void k_planar_to_aos(const float* __restrict__ planar, int64_t pitch, int64_t n, int C,
-                                double* __restrict__ aos) {
+                                A* __restrict__ aos) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  for (int c = 0; c < C; ++c) aos[i * C + c] = (double)planar[c * pitch + i];
+  for (int c = 0; c < C; ++c) aos[i * C + c] = (A)planar[c * pitch + i];
 }
 
 __global__ void k_mask_u8(const double* __restrict__ m, int64_t n, uint8_t* __restrict__ out) {
@@ -442,6 +444,71 @@ void par_memcpy(char* dst, const char* src, size_t n) {
   for (auto& t : th) t.join();
 }
 
+// Model parameters cross the bus as fp32 (what the device stores): the host
+// side converts double <-> float in parallel while the pinned chunks are in
+// flight, halving the bytes a pageable double copy would move. The rounding
+// is the device's own cast (round to nearest), so results are unchanged.
+}  // namespace
+}  // extern "C"
+namespace {
+template <class H, class D>
+void par_convert(D* dst, const H* src, size_t n) {
+  const size_t kMin = size_t(1) << 18;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nt = std::min<size_t>({(size_t)std::min(hw, 16u), (n + kMin - 1) / kMin});
+  if (nt <= 1) {
+    for (size_t i = 0; i < n; ++i) dst[i] = (D)src[i];
+    return;
+  }
+  const size_t per = (n + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (size_t o = 0; o < n; o += per)
+    th.emplace_back([=] {
+      const size_t e = std::min(n, o + per);
+      for (size_t i = o; i < e; ++i) dst[i] = (D)src[i];
+    });
+  for (auto& t : th) t.join();
+}
+}  // namespace
+extern "C" {
+namespace {
+
+void staged_params(dsg_ctx ctx, double* host, float* dev, size_t count, bool to_host) {
+  constexpr size_t kChunk = size_t(8) << 20;  // floats per pinned chunk (32 MiB)
+  cudaStream_t st = ctx->stream;
+  for (int k = 0; k < 2; ++k) {
+    if (!ctx->pin[k]) DSG_CUDA_CHECK(cudaMallocHost(&ctx->pin[k], size_t(32) << 20));
+    if (!ctx->pin_ev[k]) DSG_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->pin_ev[k], cudaEventDisableTiming));
+  }
+  float* pin[2] = {reinterpret_cast<float*>(ctx->pin[0]), reinterpret_cast<float*>(ctx->pin[1])};
+  const size_t nch = (count + kChunk - 1) / kChunk;
+  auto len = [&](size_t k) { return std::min(kChunk, count - k * kChunk); };
+  if (to_host) {
+    DSG_CUDA_CHECK(cudaMemcpyAsync(pin[0], dev, sizeof(float) * len(0), cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaEventRecord(ctx->pin_ev[0], st));
+    for (size_t k = 0; k < nch; ++k) {
+      if (k + 1 < nch) {
+        const int b = (int)((k + 1) & 1);
+        DSG_CUDA_CHECK(cudaMemcpyAsync(pin[b], dev + (k + 1) * kChunk, sizeof(float) * len(k + 1),
+                                       cudaMemcpyDeviceToHost, st));
+        DSG_CUDA_CHECK(cudaEventRecord(ctx->pin_ev[b], st));
+      }
+      DSG_CUDA_CHECK(cudaEventSynchronize(ctx->pin_ev[k & 1]));
+      par_convert<float, double>(host + k * kChunk, pin[k & 1], len(k));
+    }
+  } else {
+    for (size_t k = 0; k < nch; ++k) {
+      const int b = (int)(k & 1);
+      if (k >= 2) DSG_CUDA_CHECK(cudaEventSynchronize(ctx->pin_ev[b]));
+      par_convert<double, float>(pin[b], host + k * kChunk, len(k));
+      DSG_CUDA_CHECK(cudaMemcpyAsync(dev + k * kChunk, pin[b], sizeof(float) * len(k),
+                                     cudaMemcpyHostToDevice, st));
+      DSG_CUDA_CHECK(cudaEventRecord(ctx->pin_ev[b], st));
+    }
+  }
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+}
+
 void staged_copy(dsg_ctx ctx, char* host, char* dev, size_t bytes, bool to_host) {
   constexpr size_t kChunk = size_t(32) << 20;
   cudaStream_t st = ctx->stream;
@@ -495,9 +562,8 @@ int dsg_model_upload(dsg_ctx ctx, dsg_model model, const double* params, int64_t
     m.iteration = iteration;
     m.origin_partition = origin_partition;
     if (n > 0) {
-      double* st = ctx->stage_d.ensure(kParams * n);
-      staged_copy(ctx, (char*)const_cast<double*>(params), (char*)st, sizeof(double) * kParams * n,
-                  false);
+      float* st = ctx->stage_f.ensure(kParams * n);
+      staged_params(ctx, const_cast<double*>(params), st, (size_t)kParams * n, false);
       k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
       count_launch();
     }
@@ -514,9 +580,8 @@ int dsg_model_set_params(dsg_ctx ctx, dsg_model model, const double* params, int
     DeviceGuard g(ctx->device);
     m.iteration = iteration;
     if (n > 0) {
-      double* st = ctx->stage_d.ensure(kParams * n);
-      staged_copy(ctx, (char*)const_cast<double*>(params), (char*)st, sizeof(double) * kParams * n,
-                  false);
+      float* st = ctx->stage_f.ensure(kParams * n);
+      staged_params(ctx, const_cast<double*>(params), st, (size_t)kParams * n, false);
       k_aos_to_planar<<<nblk(n), 256, 0, ctx->stream>>>(st, n, kParams, m.params.get(), m.cap);
       count_launch();
     }
@@ -534,10 +599,10 @@ int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t cap
     if (origin_partition) *origin_partition = m.origin_partition;
     if (!params || m.n == 0) return;
     if (capacity < m.n) fail(kInvalidArgument, "output capacity too small");
-    double* st = ctx->stage_d.ensure(kParams * m.n);
+    float* st = ctx->stage_f.ensure(kParams * m.n);
     k_planar_to_aos<<<nblk(m.n), 256, 0, ctx->stream>>>(m.params.get(), m.cap, m.n, kParams, st);
     count_launch();
-    staged_copy(ctx, (char*)params, (char*)st, sizeof(double) * kParams * m.n, true);
+    staged_params(ctx, params, st, (size_t)kParams * m.n, true);
   });
 }
 
