@@ -20,10 +20,10 @@
 //   seed_gaussians / median_nn_spacing / ground_truth_model
 //                     seed.hpp:49 / :39 / :78       dsplat::b200::...
 //   partition_cloud   partition.hpp:42              dsplat::b200::partition_cloud
+//   merge_models      partition.hpp:109             dsplat::b200::merge_models
+//     (device-resident models: dsg_merge_models / dsg_merge_allgather)
 //   build_orbital_cameras, split_rig, owns: host-side, unchanged from the
-//     reference (camera.hpp:75-130, partition.hpp:34-40). merge_models of
-//     device-resident models is dsg_merge_models / dsg_merge_allgather in the
-//     C ABI (the trained models never leave the GPU).
+//     reference (camera.hpp:75-130, partition.hpp:34-40).
 //
 // Errors: every failing call throws dsplat::Error with the same ErrorCode and
 // what() text ("<Code>: msg") the reference throws (error.hpp:57-61).
@@ -384,6 +384,101 @@ inline std::vector<double> knn_mean_distances(const PointCloud& pc, int k) {
     check(dsg_knn_mean(Context::current().get(), pts.data(), static_cast<int64_t>(pc.size()), k,
                        out.data()));
   return out;
+}
+
+namespace detail {
+inline void cloud_arrays(const PointCloud& pc, std::vector<double>& pts, std::vector<double>& col) {
+  pts.resize(3 * pc.size());
+  col.resize(3 * pc.size());
+  for (size_t i = 0; i < pc.size(); ++i) {
+    const SurfacePoint& p = pc.points[i];
+    pts[3 * i] = p.position.x;
+    pts[3 * i + 1] = p.position.y;
+    pts[3 * i + 2] = p.position.z;
+    col[3 * i] = p.color.x;
+    col[3 * i + 1] = p.color.y;
+    col[3 * i + 2] = p.color.z;
+  }
+}
+
+inline SplatModel download(Context& ctx, dsg_model h) {
+  int64_t n = 0, it = 0, st = 0;
+  check(dsg_model_info(h, &n, &it, &st));
+  std::vector<double> p(14 * static_cast<size_t>(n));
+  int32_t op = -1;
+  check(dsg_model_download(ctx.get(), h, p.data(), n, &n, &it, &op));
+  SplatModel m;
+  params_to(p, m);
+  m.iteration = it;
+  if (op >= 0) m.origin_partition = op;
+  return m;
+}
+}  // namespace detail
+
+// seed_gaussians (seed.hpp:49-74): exact fp64 kNN scales, parameters stored
+// (and returned) at the device's fp32 precision.
+inline SplatModel seed_gaussians(const PointCloud& pc, ScaleRule rule, int k = 3,
+                                 double fixed_scale = 0.01) {
+  if (pc.empty()) throw Error(ErrorCode::EmptyCloud, "cannot seed from an empty cloud");
+  Context& ctx = Context::current();
+  std::vector<double> pts, col;
+  detail::cloud_arrays(pc, pts, col);
+  dsg_model h = nullptr;
+  check(dsg_model_create(ctx.get(), &h));
+  std::unique_ptr<dsg_model_s, int (*)(dsg_model)> guard(h, dsg_model_destroy);
+  check(dsg_seed_gaussians(ctx.get(), pts.data(), col.data(), static_cast<int64_t>(pc.size()),
+                           rule == ScaleRule::Knn ? 0 : 1, k, fixed_scale, h));
+  return detail::download(ctx, h);
+}
+
+// ground_truth_model (seed.hpp:78-94), fp32 parameters as above.
+inline SplatModel ground_truth_model(const PointCloud& pc, double scale_world,
+                                     double opacity = 0.97) {
+  if (pc.empty()) throw Error(ErrorCode::EmptyCloud, "cannot build ground truth from nothing");
+  Context& ctx = Context::current();
+  std::vector<double> pts, col;
+  detail::cloud_arrays(pc, pts, col);
+  dsg_model h = nullptr;
+  check(dsg_model_create(ctx.get(), &h));
+  std::unique_ptr<dsg_model_s, int (*)(dsg_model)> guard(h, dsg_model_destroy);
+  check(dsg_ground_truth_model(ctx.get(), pts.data(), col.data(), static_cast<int64_t>(pc.size()),
+                               scale_world, opacity, h));
+  return detail::download(ctx, h);
+}
+
+// merge_models (partition.hpp:109-126) on the device. The device holds
+// parameters as fp32, so the result equals the reference's for the fp32
+// models training produces (ownership is tested on the stored mu against the
+// fp64 cuts, exactly as `owns`).
+inline SplatModel merge_models(const std::vector<SplatModel>& models,
+                               const std::vector<Partition>& partitions) {
+  if (models.size() != partitions.size())
+    throw Error(ErrorCode::MismatchedCounts, "one model per partition required");
+  for (size_t k = 0; k < models.size(); ++k) {
+    if (!models[k].origin_partition.has_value())
+      throw Error(ErrorCode::MismatchedCounts, "model missing origin partition id");
+    if (*models[k].origin_partition != partitions[k].id)
+      throw Error(ErrorCode::MismatchedCounts, "model/partition id mismatch");
+  }
+  Context& ctx = Context::current();
+  std::vector<std::unique_ptr<detail::DeviceModel>> dms;
+  std::vector<dsg_model> hs;
+  std::vector<double> lo, hi;
+  for (size_t k = 0; k < models.size(); ++k) {
+    dms.push_back(std::make_unique<detail::DeviceModel>(models[k], ctx));
+    hs.push_back(dms.back()->h);
+    lo.push_back(partitions[k].cut_lo);
+    hi.push_back(partitions[k].cut_hi);
+  }
+  dsg_model out = nullptr;
+  check(dsg_model_create(ctx.get(), &out));
+  std::unique_ptr<dsg_model_s, int (*)(dsg_model)> guard(out, dsg_model_destroy);
+  const int axis = partitions.empty() ? 0 : partitions[0].cut_axis;
+  check(dsg_merge_models(ctx.get(), hs.data(), static_cast<int32_t>(hs.size()), axis, lo.data(),
+                         hi.data(), out));
+  SplatModel m = detail::download(ctx, out);
+  m.origin_partition.reset();
+  return m;
 }
 
 // partition_cloud (partition.hpp:42-104): cuts, owned boxes and ownership /

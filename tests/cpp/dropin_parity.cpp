@@ -174,6 +174,57 @@ int main() {
     } catch (const Error& e) {
       EXPECT(e.code() == ErrorCode::EmptyCloud, "code %d", (int)e.code());
     }
+    // seeds / ground truth: the reference values rounded to fp32
+    {
+      PointCloud small;
+      small.points.assign(pc.points.begin(), pc.points.begin() + 600);
+      const SplatModel sa = seed_gaussians(small, ScaleRule::Knn, 3);
+      const SplatModel sb = b200::seed_gaussians(small, ScaleRule::Knn, 3);
+      const SplatModel ga = ground_truth_model(small, 0.01, 0.97);
+      const SplatModel gb = b200::ground_truth_model(small, 0.01, 0.97);
+      EXPECT(sa.size() == sb.size() && ga.size() == gb.size(), "seed sizes");
+      // relative error within fp32 rounding (device fp64 log may differ from
+      // glibc's by an ulp before the fp32 rounding)
+      double serr = 0;
+      auto rel = [](double a, double b) { return std::abs(a - b) / std::max(std::abs(a), 1e-30); };
+      for (size_t i = 0; i < sa.size() && i < sb.size(); ++i) {
+        serr = std::max(serr, rel(sa.gaussians[i].log_scale.x, sb.gaussians[i].log_scale.x));
+        serr = std::max(serr, rel(sa.gaussians[i].opacity_logit, sb.gaussians[i].opacity_logit));
+        serr = std::max(serr, rel(ga.gaussians[i].log_scale.y, gb.gaussians[i].log_scale.y));
+        serr = std::max(serr, rel(ga.gaussians[i].mu.z, gb.gaussians[i].mu.z));
+      }
+      EXPECT(serr <= 2e-7, "seed/gt values differ by %g relative", serr);
+    }
+    // merge_models on fp32-exact models: identical to the reference
+    {
+      auto parts = partition_cloud(pc, 3, 0.1);
+      std::vector<SplatModel> models;
+      for (int k = 0; k < 3; ++k) {
+        SplatModel m = scene(300 + k, 200 + 50 * k, 1.0);
+        for (auto& g : m.gaussians) {  // spread over the cut axis range
+          g.mu.z = f32(g.mu.z * 4.0);
+        }
+        m.origin_partition = k;
+        m.iteration = 10 + k;
+        models.push_back(m);
+      }
+      const SplatModel ma = merge_models(models, parts);
+      const SplatModel mb = b200::merge_models(models, parts);
+      EXPECT(ma.size() == mb.size(), "merge size %zu vs %zu", ma.size(), mb.size());
+      EXPECT(ma.iteration == mb.iteration, "merge iteration");
+      bool same = ma.size() == mb.size();
+      for (size_t i = 0; same && i < ma.size(); ++i)
+        same = ma.gaussians[i].mu == mb.gaussians[i].mu &&
+               ma.gaussians[i].opacity_logit == mb.gaussians[i].opacity_logit;
+      EXPECT(same, "merged splats differ");
+      try {
+        models[1].origin_partition = 2;
+        b200::merge_models(models, parts);
+        EXPECT(false, "MismatchedCounts not thrown");
+      } catch (const Error& e) {
+        EXPECT(e.code() == ErrorCode::MismatchedCounts, "merge code %d", (int)e.code());
+      }
+    }
   }
   std::printf("dropin_parity: %d failure(s)\n", failures);
   return failures;
