@@ -348,17 +348,20 @@ __global__ void k_unit_counts(const uint2* __restrict__ ranges, const uint32_t* 
 // tile i = unit nt + (base[i] - i) + k - 1 (base[i] - i = later segments of
 // earlier tiles); first_of maps a later unit back to its tile's first unit.
 __global__ void k_unit_fill(const uint2* __restrict__ ranges, const uint32_t* __restrict__ order,
-                            int nt, uint32_t seg, const uint32_t* __restrict__ base,
+                            int nt, uint32_t seg, uint32_t split_len,
+                            const uint32_t* __restrict__ base,
                             uint4* __restrict__ units, uint32_t* __restrict__ first_of) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint32_t t = order[i];
   const uint2 r = ranges[t];
   const uint32_t b = base[i], nseg = base[i + 1] - b;
+  // split: even the forward walks the segments in parallel (blend.cu)
+  const uint32_t split = nseg > 1 && r.y - r.x > split_len ? 1u << 31 : 0u;
   for (uint32_t k = 0; k < nseg; ++k) {
     const uint32_t beg = r.x + k * seg, end = min(r.y, beg + seg);
     const uint32_t u = k == 0 ? (uint32_t)i : (uint32_t)nt + (b - i) + k - 1;
-    units[u] = make_uint4(t, beg, end, k | (nseg << 16));
+    units[u] = make_uint4(t, beg, end, k | (nseg << 16) | split);
     if (k > 0) first_of[u - nt] = (uint32_t)i;
   }
 }
@@ -554,6 +557,10 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     // blend work units: ceil(len / seg_len) per tile in that order
     f.band_tiles = nt;
     f.unit_cap = nt + (int64_t)nd / f.seg_len + 1;
+    // forward splitting only for lists far beyond what termination usually
+    // cuts short (the split forward re-walks later segments' products)
+    f.split_len = std::max<int64_t>(kSplitMin, kSplitFactor * f.seg_len);
+    f.split_cap = (int64_t)nd > f.split_len ? (int64_t)nd / f.split_len + 1 : 0;
     f.units.ensure(f.unit_cap);
     f.unit_base.ensure(nt + 1);
     f.nonlast.ensure(std::max<int64_t>(f.unit_cap - nt, 1));
@@ -564,7 +571,8 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     count_launch();
     exclusive_scan_u32(ucnt, f.unit_base.get(), nt, f.scan, st);
     k_unit_fill<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), f.tile_order.get(), nt,
-                                                 (uint32_t)f.seg_len, f.unit_base.get(),
+                                                 (uint32_t)f.seg_len, (uint32_t)f.split_len,
+                                                 f.unit_base.get(),
                                                  f.units.get(), f.nonlast.get());
     count_launch();
   }

@@ -17,7 +17,16 @@ constexpr int kSegMin = DSG_SEG_MIN;
 #define DSG_SEG_DIV 512
 #endif
 constexpr int kSegDiv = DSG_SEG_DIV;
-constexpr int kUnitPlanes = 7;  // per-unit per-pixel planes (blend.cu UnitPlane)
+constexpr int kUnitPlanes = 14;  // per-unit per-pixel planes (blend.cu UnitPlane)
+#ifndef DSG_SPLIT_MIN
+#define DSG_SPLIT_MIN 32768
+#endif
+#ifndef DSG_SPLIT_FACTOR
+#define DSG_SPLIT_FACTOR 4
+#endif
+// the forward splits lists longer than max(kSplitMin, kSplitFactor * seg_len)
+constexpr int64_t kSplitMin = DSG_SPLIT_MIN;
+constexpr int64_t kSplitFactor = DSG_SPLIT_FACTOR;
 
 struct PreprocessArgs {
   const float* params;  // [14][pitch] planar fp32 model
@@ -65,7 +74,7 @@ struct Frame {
   DevBuf<uint32_t> unit_base;  // [band tiles + 1] first unit of each ordered tile; [nt] = total
   DevBuf<uint32_t> nonlast;    // units that are not their tile's last segment
   DevBuf<float> ubuf;          // per unit, per pixel segment state (blend.cu UnitPlane)
-  int64_t unit_cap = 0, band_tiles = 0, seg_len = kSegMin;
+  int64_t unit_cap = 0, band_tiles = 0, seg_len = kSegMin, split_len = 0, split_cap = 0;
   DevBuf<uint32_t> counters;
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL;

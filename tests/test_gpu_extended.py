@@ -222,3 +222,37 @@ def test_near_coincident_depth_order(orc, ctx, cluster):
     b = orc.render(model, cam, RenderConfig())
     np.testing.assert_array_equal(a.splat_order, b.splat_order)
     assert np.max(np.abs(a.color - b.color)) <= 1e-3
+
+
+@pytest.mark.parametrize("opacity", [-2.0, 1.5])
+def test_long_tile_lists_split(orc, ctx, opacity):
+    """A tile list of ~60k entries: the forward splits it into segments
+    (segment products, incoming T, exact termination) and the backward walks
+    them in parallel from checkpoints. Images, contributor counts and
+    gradients follow the oracle; low opacity keeps most pixels alive through
+    every segment, high opacity terminates them in the first one."""
+    rng = np.random.default_rng(11)
+    n = 60000
+    p = np.zeros((n, 14))
+    cam = make_camera(64)
+    # tiny splats packed into a few tiles around the image centre
+    p[:, 0] = rng.uniform(-0.02, 0.02, n)
+    p[:, 1] = rng.uniform(-0.02, 0.02, n)
+    p[:, 2] = rng.uniform(-0.3, 0.3, n)
+    p[:, 3:6] = np.log(rng.uniform(0.001, 0.004, (n, 3)))
+    q = rng.normal(size=(n, 4))
+    p[:, 6:10] = q / np.linalg.norm(q, axis=1, keepdims=True)
+    p[:, 10] = opacity + rng.uniform(-0.5, 0.5, n)
+    p[:, 11:14] = rng.uniform(0.1, 0.9, (n, 3))
+    model = fp32_exact(SplatModel(p))
+    counts, _ = api.bin_splats(model, cam, RenderConfig(), ctx=ctx, capacity=1 << 22)
+    assert counts.max() > 40000  # the forward splits lists above 32768
+    a = api.render(model, cam, RenderConfig(), ctx=ctx)
+    b = orc.render(model, cam, RenderConfig())
+    assert np.max(np.abs(a.color - b.color)) <= 1e-3
+    nc_a, nc_b = np.asarray(a.per_pixel_contributor_count), np.asarray(b.per_pixel_contributor_count)
+    assert np.sum(nc_a != nc_b) <= 3 and np.max(np.abs(nc_a - nc_b)) <= 1
+    dl = np.random.default_rng(2).normal(size=a.color.shape) * 0.01
+    ga = api.backward(model, cam, RenderConfig(), a, dl, ctx=ctx)
+    gb = orc.backward(model, cam, RenderConfig(), b, dl)
+    assert_grads_close(ga.grads, gb.grads)
