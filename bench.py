@@ -243,7 +243,7 @@ def train_config(args, rank: int, iterations: int) -> TrainConfig:
 
 KERNEL_OF_STAGE = {"preprocess": "k_preprocess", "depth_sort": "k_onesweep (depth)",
                    "scan_duplicate": "k_duplicate", "tile_sort_ranges": "k_onesweep (tile)",
-                   "blend_fwd": "k_blend_fwd", "loss": "k_ssim_stats+k_loss_grad",
+                   "blend_fwd": "k_blend_fwd<0>", "loss": "k_ssim_stats+k_loss_grad",
                    "blend_bwd": "k_blend_bwd", "chain": "k_chain", "adam": "k_adam"}
 
 

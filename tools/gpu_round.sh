@@ -21,7 +21,7 @@ ncu --nvtx --nvtx-include "dsg_timed/" --metrics gpu__time_duration.sum --clock-
 echo "ncu launch rc=$?"
 # full capture: one launch of each step kernel inside the timed region
 ncu --nvtx --nvtx-include "dsg_timed/" --set full --clock-control none --import-source on \
-    -k regex:"k_blend_bwd|k_blend_fwd|k_chain|k_adam|k_preprocess|k_onesweep" -c 9 \
+    -k regex:"k_blend_bwd|k_blend_fwd|k_chain|k_adam|k_preprocess|k_onesweep|k_duplicate" -c 16 \
     -o "$out/${tag}_step_full" -f \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-global \
     > "$out/${tag}_ncu_full.log" 2>&1

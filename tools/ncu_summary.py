@@ -1,4 +1,5 @@
-"""Summarise an `ncu --set full` report (one launch per kernel) into a
+"""Summarise `ncu --set full` reports (one launch per kernel; several reports
+comma-separated) into a
 markdown table and profiles/traffic.json (DRAM bytes per launch, read by
 bench.py for roofline.traffic).
 
@@ -36,13 +37,19 @@ def short(name: str) -> str:
     return name.replace("void ", "")
 
 
-def main(rep: str, tag: str, command: str):
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True, check=True).stdout
-    rows = list(csv.reader(io.StringIO(raw)))
+def main(reps: str, tag: str, command: str):
+    seen, table, traffic = {}, [], {}
+    for rep in reps.split(","):
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True, check=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        summarise(rows, seen, table, traffic, tag)
+    write(tag, command, table, traffic)
+
+
+def summarise(rows, seen, table, traffic, tag):
     hdr, units = rows[0], rows[1]
     ki = hdr.index("Kernel Name")
-    seen, table, traffic = {}, [], {}
     for r in rows[2:]:
         k = short(r[ki])
         seen[k] = seen.get(k, 0) + 1
@@ -56,6 +63,9 @@ def main(rep: str, tag: str, command: str):
         table.append((k, vals))
         traffic[k] = {"dram_bytes_per_launch": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
                       "source": f"profiles/{tag}_ncu_step.md"}
+
+
+def write(tag, command, table, traffic):
     lines = [f"# {tag}: ncu --set full, one launch per step kernel", "",
              f"Command: `{command}`", "",
              "Cold-cache, serialised replay with clocks unlocked (`--clock-control none`): compare "
