@@ -283,6 +283,8 @@ def roofline(stage_ms, n, nv, npix, n_dup, peak, peak_kind):
         if tr:
             out["traffic"] = float(tr["dram_bytes_per_launch"])
             out["traffic_source"] = tr["source"]
+            if "issue_active_pct" in tr:  # the bound that applies to the blend kernels
+                out["issue_slots_busy_frac"] = round(float(tr["issue_active_pct"]) / 100.0, 3)
     except (OSError, ValueError, KeyError):
         pass
     if dom in ("blend_fwd", "blend_bwd"):

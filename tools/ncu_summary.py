@@ -62,6 +62,7 @@ def summarise(rows, seen, table, traffic, tag):
             vals[m] = v * SCALE.get(units[i], 1.0) if units[i] in SCALE else v
         table.append((k, vals))
         traffic[k] = {"dram_bytes_per_launch": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
+                      "issue_active_pct": vals["smsp__issue_active.avg.pct_of_peak_sustained_active"],
                       "source": f"profiles/{tag}_ncu_step.md"}
 
 
