@@ -13,6 +13,7 @@
 // then stably sorted by tile id, so every tile list is in reference
 // compositing order.
 #include <atomic>
+#include <cstdlib>
 
 #include "dsg_internal.h"
 #include "raster.h"
@@ -370,14 +371,18 @@ __global__ void k_unit_fill(const uint2* __restrict__ ranges, const uint32_t* __
 // floor(log2(list length)) and emitted heaviest bucket first, so the long
 // lists start early instead of forming the tail (order inside a bucket is
 // irrelevant: tiles are independent).
+constexpr int kBins = 35;  // 0..32: floor(log2 len) + 1; 33: > seg_len; 34: > split_len
+
 __global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t seg,
-                            uint32_t* bins, uint32_t* counts) {
+                            uint32_t split, uint32_t* bins, uint32_t* counts) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint2 r = ranges[t0 + i];
   const uint32_t len = r.y - r.x;
-  // bin 33 = multi-segment lists (len > seg): they lead the order
-  const uint32_t b = len > seg ? 33u : (len ? 32u - __clz(len) : 0u);
+  // bin 34 = split lists (len > split_len), then bin 33 = other multi-segment
+  // lists (len > seg): they lead the order, so the split tiles are the first
+  // units (at most split_cap of them)
+  const uint32_t b = len > split ? 34u : len > seg ? 33u : (len ? 32u - __clz(len) : 0u);
   bins[i] = b;
   atomicAdd(&counts[b], 1u);
 }
@@ -385,7 +390,7 @@ __global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, ui
 __global__ void k_tile_bin_offsets(uint32_t* counts) {  // one warp: descending exclusive scan
   const int lane = threadIdx.x;
   uint32_t run = 0;
-  for (int b = 33; b >= 0; --b) {
+  for (int b = kBins - 1; b >= 0; --b) {
     const uint32_t c = counts[b];
     if (lane == 0) counts[b] = run;
     run += c;
@@ -543,13 +548,23 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     const int t0 = cam.band_ty0 * cam.tiles_x;
     const int nt = (cam.band_ty1 - cam.band_ty0) * cam.tiles_x;
     f.tile_order.ensure(std::max(nt, 1));
-    f.tile_bins.ensure(std::max(nt, 1) + 34);
+    f.tile_bins.ensure(std::max(nt, 1) + kBins);
     uint32_t* counts = f.tile_bins.get() + std::max(nt, 1);
-    DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, 34 * sizeof(uint32_t), st));
+    DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, kBins * sizeof(uint32_t), st));
     f.seg_len = std::max<int64_t>(kSegMin, ((int64_t)nd + kSegDiv - 1) / kSegDiv);
     f.seg_len = (f.seg_len + 31) & ~int64_t(31);  // whole 32-entry chunks
+    // forward splitting only for lists far beyond what termination usually
+    // cuts short (the split forward re-walks later segments' products)
+    f.split_len = std::max<int64_t>(kSplitMin, kSplitFactor * f.seg_len);
+    static const int64_t split_env = [] {  // DSG_SPLIT_LEN: tuning override
+      const char* e = std::getenv("DSG_SPLIT_LEN");
+      return e ? std::max<int64_t>(std::atoll(e), 0) : int64_t(0);
+    }();
+    if (split_env > 0) f.split_len = std::max<int64_t>(split_env, f.seg_len);
+    f.split_cap = (int64_t)nd > f.split_len ? (int64_t)nd / f.split_len + 1 : 0;
     k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, (uint32_t)f.seg_len,
-                                                 f.tile_bins.get(), counts);
+                                                 (uint32_t)f.split_len, f.tile_bins.get(),
+                                                 counts);
     k_tile_bin_offsets<<<1, 32, 0, st>>>(counts);
     k_tile_order<<<blocks(nt, 256), 256, 0, st>>>(f.tile_bins.get(), t0, nt, counts,
                                                   f.tile_order.get());
@@ -557,10 +572,6 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     // blend work units: ceil(len / seg_len) per tile in that order
     f.band_tiles = nt;
     f.unit_cap = nt + (int64_t)nd / f.seg_len + 1;
-    // forward splitting only for lists far beyond what termination usually
-    // cuts short (the split forward re-walks later segments' products)
-    f.split_len = std::max<int64_t>(kSplitMin, kSplitFactor * f.seg_len);
-    f.split_cap = (int64_t)nd > f.split_len ? (int64_t)nd / f.split_len + 1 : 0;
     f.units.ensure(f.unit_cap);
     f.unit_base.ensure(nt + 1);
     f.nonlast.ensure(std::max<int64_t>(f.unit_cap - nt, 1));

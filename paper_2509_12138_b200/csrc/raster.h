@@ -92,6 +92,32 @@ struct Frame {
   DevBuf<double> loss_out;
   SortScratch sort;
   ScanScratch scan;
+  // high-priority side stream for the split-tile forward, which runs beside
+  // the main forward kernel (created on first use, on the frame's device)
+  struct Side {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t get() {
+      if (!s) {
+        int lo = 0, hi = 0;
+        DSG_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        DSG_CUDA_CHECK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, hi));
+        DSG_CUDA_CHECK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+        DSG_CUDA_CHECK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+      }
+      return s;
+    }
+    Side() = default;
+    Side(const Side&) = delete;
+    Side& operator=(const Side&) = delete;
+    ~Side() {
+      if (s) {
+        cudaEventDestroy(fork);
+        cudaEventDestroy(join);
+        cudaStreamDestroy(s);
+      }
+    }
+  } side;
 };
 
 // Model tensors on device (planar [14][cap] fp32 for params/grads/moments).
