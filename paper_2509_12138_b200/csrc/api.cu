@@ -376,6 +376,12 @@ int dsg_ctx_create(int32_t device, dsg_ctx* out) {
     c->device = device;
     DeviceGuard g(device);
     DSG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    // the two 32 MiB pinned staging chunks of large model transfers are part
+    // of the context (pinning them costs tens of ms on a cold host)
+    for (int k = 0; k < 2; ++k) {
+      DSG_CUDA_CHECK(cudaMallocHost(&c->pin[k], size_t(32) << 20));
+      DSG_CUDA_CHECK(cudaEventCreateWithFlags(&c->pin_ev[k], cudaEventDisableTiming));
+    }
     *out = c;
   });
 }

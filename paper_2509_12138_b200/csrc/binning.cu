@@ -368,21 +368,27 @@ __global__ void k_unit_fill(const uint2* __restrict__ ranges, const uint32_t* __
 }
 
 // Longest-first tile schedule for the blend kernels: tiles are bucketed by
-// floor(log2(list length)) and emitted heaviest bucket first, so the long
-// lists start early instead of forming the tail (order inside a bucket is
-// irrelevant: tiles are independent).
-constexpr int kBins = 35;  // 0..32: floor(log2 len) + 1; 33: > seg_len; 34: > split_len
+// list length in quarter octaves (floor(4 log2 len)) and emitted heaviest
+// bucket first, so the long lists start early instead of forming the tail
+// (order inside a bucket is irrelevant: tiles are independent). Split lists
+// (len > split_len) form the top bucket, so they are the first units (at
+// most split_cap of them) and the split forward's per-tile grids cover them.
+constexpr int kBins = 4 * 32 + 2;
 
-__global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t seg,
-                            uint32_t split, uint32_t* bins, uint32_t* counts) {
+__global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t split,
+                            uint32_t* bins, uint32_t* counts) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint2 r = ranges[t0 + i];
   const uint32_t len = r.y - r.x;
-  // bin 34 = split lists (len > split_len), then bin 33 = other multi-segment
-  // lists (len > seg): they lead the order, so the split tiles are the first
-  // units (at most split_cap of them)
-  const uint32_t b = len > split ? 34u : len > seg ? 33u : (len ? 32u - __clz(len) : 0u);
+  uint32_t b = 0;
+  if (len > split) {
+    b = kBins - 1;
+  } else if (len) {
+    const uint32_t e = 31u - __clz(len);                      // floor(log2 len)
+    const uint32_t q = e >= 2 ? (len >> (e - 2)) & 3u : (len << (2 - e)) & 3u;
+    b = 1u + 4u * e + q;                                      // 1 .. 128
+  }
   bins[i] = b;
   atomicAdd(&counts[b], 1u);
 }
@@ -552,6 +558,11 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     uint32_t* counts = f.tile_bins.get() + std::max(nt, 1);
     DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, kBins * sizeof(uint32_t), st));
     f.seg_len = std::max<int64_t>(kSegMin, ((int64_t)nd + kSegDiv - 1) / kSegDiv);
+    static const int64_t seg_env = [] {  // DSG_SEG_LEN: tuning override
+      const char* e = std::getenv("DSG_SEG_LEN");
+      return e ? std::max<int64_t>(std::atoll(e), 0) : int64_t(0);
+    }();
+    if (seg_env > 0) f.seg_len = seg_env;
     f.seg_len = (f.seg_len + 31) & ~int64_t(31);  // whole 32-entry chunks
     // forward splitting only for lists far beyond what termination usually
     // cuts short (the split forward re-walks later segments' products)
@@ -562,9 +573,8 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     }();
     if (split_env > 0) f.split_len = std::max<int64_t>(split_env, f.seg_len);
     f.split_cap = (int64_t)nd > f.split_len ? (int64_t)nd / f.split_len + 1 : 0;
-    k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, (uint32_t)f.seg_len,
-                                                 (uint32_t)f.split_len, f.tile_bins.get(),
-                                                 counts);
+    k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, (uint32_t)f.split_len,
+                                                 f.tile_bins.get(), counts);
     k_tile_bin_offsets<<<1, 32, 0, st>>>(counts);
     k_tile_order<<<blocks(nt, 256), 256, 0, st>>>(f.tile_bins.get(), t0, nt, counts,
                                                   f.tile_order.get());

@@ -10,11 +10,11 @@ namespace dsg {
 // the kernel's tail: segment length = max(kSegMin, n_dup / kSegDiv), i.e. a
 // list longer than the average work of ~kSegDiv/8 concurrent warps.
 #ifndef DSG_SEG_MIN
-#define DSG_SEG_MIN 2048
+#define DSG_SEG_MIN 1024
 #endif
 constexpr int kSegMin = DSG_SEG_MIN;
 #ifndef DSG_SEG_DIV
-#define DSG_SEG_DIV 512
+#define DSG_SEG_DIV 8192
 #endif
 constexpr int kSegDiv = DSG_SEG_DIV;
 constexpr int kUnitPlanes = 14;  // per-unit per-pixel planes (blend.cu UnitPlane)
