@@ -10,7 +10,7 @@ namespace dsg {
 // the kernel's tail: segment length = max(kSegMin, n_dup / kSegDiv), i.e. a
 // list longer than the average work of ~kSegDiv/8 concurrent warps.
 #ifndef DSG_SEG_MIN
-#define DSG_SEG_MIN 1024
+#define DSG_SEG_MIN 256
 #endif
 constexpr int kSegMin = DSG_SEG_MIN;
 #ifndef DSG_SEG_DIV
