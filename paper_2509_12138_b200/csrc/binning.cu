@@ -557,7 +557,16 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     f.tile_bins.ensure(std::max(nt, 1) + kBins);
     uint32_t* counts = f.tile_bins.get() + std::max(nt, 1);
     DSG_CUDA_CHECK(cudaMemsetAsync(counts, 0, kBins * sizeof(uint32_t), st));
-    f.seg_len = std::max<int64_t>(kSegMin, ((int64_t)nd + kSegDiv - 1) / kSegDiv);
+    // A frame whose tiles alone cannot fill the GPU (config 1: 256 tiles at
+    // 256^2) gets shorter units and splits its long lists in the forward too;
+    // a full frame keeps the forward's single walk (its dense tiles terminate
+    // early, which the split forward cannot exploit).
+    int dev = 0, sms = 148;
+    DSG_CUDA_CHECK(cudaGetDevice(&dev));
+    DSG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const bool underfilled = (int64_t)nt * 8 < (int64_t)sms * 4 * 28;  // 8 warps/tile
+    f.seg_len = std::max<int64_t>(underfilled ? kSegMin / 2 : kSegMin,
+                                  ((int64_t)nd + kSegDiv - 1) / kSegDiv);
     static const int64_t seg_env = [] {  // DSG_SEG_LEN: tuning override
       const char* e = std::getenv("DSG_SEG_LEN");
       return e ? std::max<int64_t>(std::atoll(e), 0) : int64_t(0);
@@ -566,7 +575,8 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     f.seg_len = (f.seg_len + 31) & ~int64_t(31);  // whole 32-entry chunks
     // forward splitting only for lists far beyond what termination usually
     // cuts short (the split forward re-walks later segments' products)
-    f.split_len = std::max<int64_t>(kSplitMin, kSplitFactor * f.seg_len);
+    f.split_len = underfilled ? kSplitFactor * f.seg_len
+                              : std::max<int64_t>(kSplitMin, kSplitFactor * f.seg_len);
     static const int64_t split_env = [] {  // DSG_SPLIT_LEN: tuning override
       const char* e = std::getenv("DSG_SPLIT_LEN");
       return e ? std::max<int64_t>(std::atoll(e), 0) : int64_t(0);
