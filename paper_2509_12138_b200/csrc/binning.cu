@@ -260,15 +260,17 @@ __device__ __forceinline__ uint32_t subtile_mask(const MaskSplat& sp, int ox, in
     }
     return m;
   }
+  const float mxh = sp.mx - 0.5f;  // exact (|mx| < 2^23): pixel x = centre - 0.5
   for (int y = ry0; y <= ry1; ++y) {
     const float dy = (((float)y + 0.5f) - sp.my) - sp.myl;
     const float h2 = (sp.qcut - dy * dy * sp.q0) * sp.inv_ixx + sp.pad;
     if (h2 < 0.f) continue;
-    const float c = (sp.mx - sp.r * dy) + sp.mxl;  // x of the row's minimum q
-    const float h = sqrtf(h2);
-    const float eps = 2e-3f + 1e-5f * (fabsf(c) + h);
+    const float c = (mxh - sp.r * dy) + sp.mxl;  // row's minimum-q centre x, minus 0.5
+    float h;  // MUFU sqrt: its ~1e-7 relative error is far inside the 1e-5 pad
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(h2));
     // pixel x (centre x + 0.5) with centre in [c - h - eps, c + h + eps]
-    const float lo = ceilf(c - h - eps - 0.5f), hi = floorf(c + h + eps - 0.5f);
+    const float t = h + (2.005e-3f + 1e-5f * (fabsf(c) + h));
+    const float lo = ceilf(c - t), hi = floorf(c + t);
     const int xl = lo < (float)cx0 ? cx0 : (int)lo;
     const int xh = hi > (float)cx1 ? cx1 : (int)hi;
     if (xl > xh) continue;
