@@ -23,6 +23,9 @@ namespace dsg {
 
 namespace {
 
+#ifndef DSG_PRE_QEFF32
+#define DSG_PRE_QEFF32 1
+#endif
 #ifndef DSG_PRE_MINB
 #define DSG_PRE_MINB 5  // 5 CTAs/SM (48 regs): measured 0.27 vs 0.30 ms
 #endif
@@ -65,12 +68,25 @@ __global__ void __launch_bounds__(256, DSG_PRE_MINB) k_preprocess(PreprocessArgs
         // Effective rect for the blend's sub-tile masks: alpha >= cutoff needs
         // o*exp(-q/2) >= c, i.e. q <= 2 ln(o/c), so only pixels with
         // |d| <= sqrt(q_eff * cov) can composite (widened by one pixel).
+#if DSG_PRE_QEFF32
+        // only bounds depend on q_eff (masks and effective rects are
+        // conservative), so fp32 log with a 1e-5 pad — two orders above its
+        // error — replaces the fp64 log
+        const double q_eff = fmin(
+            a.rd.sigma_sq,
+            (double)(2.f * logf((float)op / a.rd.alpha_cutoff_f)) * (1.0 + 1e-6) + 1e-5);
+        {  // sub-tile mask constants (see subtile_mask): ixy/ixx, 1/ixx, q0, qcut
+          const double inv = 1.0 / ixx, rr = ixy * inv;
+          a.mrow[i] = make_float4((float)rr, (float)inv, (float)(iyy - ixy * rr), (float)q_eff);
+        }
+#else
         const double q_eff = fmin(a.rd.sigma_sq, 2.0 * log(op / a.rd.alpha_cutoff));
         {  // sub-tile mask constants (see subtile_mask): ixy/ixx, 1/ixx, q0, qcut
           const double inv = 1.0 / ixx, rr = ixy * inv;
           a.mrow[i] = make_float4((float)rr, (float)inv, (float)(iyy - ixy * rr),
                                   (float)(q_eff + 1e-9 * fabs(q_eff) + 1e-12));
         }
+#endif
         if (q_eff < 0.0) {
           a.erect[i] = make_int4(1, 1, 0, 0);  // never composites anywhere
         } else {
