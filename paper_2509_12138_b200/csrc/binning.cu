@@ -243,7 +243,7 @@ __global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv
 // set is the fp64 one. With q = ixx (dx - dx*)^2 + q0 dy^2, each pixel row's
 // q <= qcut set is the x interval centred at dx* = -ixy dy / ixx with
 // half-width sqrt((qcut - q0 dy^2) / ixx). Per splat the constants are
-// formed by K1 from the fp64 values (qcut = q_eff + 1e-9 relative); per row they are evaluated
+// formed by K1 (qcut = q_eff padded by 1e-5 over its fp32 log); per row they are evaluated
 // in fp32 (mean2d as hi/lo pairs, so dy is exact to ~1e-7 relative) with the
 // half-width squared padded by 1e-5 of its maximum and the interval widened
 // by 2e-3 px plus 1e-5 relative — well above the fp32 rounding (about 1e-6
