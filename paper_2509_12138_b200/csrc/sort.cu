@@ -61,9 +61,7 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
     cur[p] = 0;
     cnt[p] = 0;
   }
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const K k = keys[i];
+  auto count = [&](const K k) {
 #pragma unroll
     for (int p = 0; p < 8; ++p) {
       if (p >= passes) break;
@@ -75,7 +73,28 @@ __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, 
       cur[p] = d;
       ++cnt[p];
     }
+  };
+  int64_t i0 = 0;
+  if constexpr (sizeof(K) == 4) {
+    if ((reinterpret_cast<uintptr_t>(keys) & 15) != 0) goto scalar;
+    // 32-bit keys: four per thread per step (16 B loads, the warp reads
+    // 512 contiguous bytes), four times fewer dependent load round trips
+    const int64_t n4 = n / 4;
+    const uint4* k4 = reinterpret_cast<const uint4*>(keys);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const uint4 q = __ldg(k4 + i);
+      count((K)q.x);
+      count((K)q.y);
+      count((K)q.z);
+      count((K)q.w);
+    }
+    i0 = n4 * 4;
   }
+scalar:
+  for (int64_t i = i0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    count(keys[i]);
 #pragma unroll
   for (int p = 0; p < 8; ++p)
     if (p < passes && cnt[p]) atomicAdd(&h[cp][p][cur[p]], cnt[p]);
