@@ -343,13 +343,36 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
 // for the blend warps).
 __global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd, uint2* ranges,
                               uint8_t* __restrict__ emask) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= nd) return;
-  const uint32_t k = tile_key[e];
-  const uint32_t t = k & kTileIdMask;
-  emask[e] = (uint8_t)(k >> kMaskShift);
-  if (e == 0 || (tile_key[e - 1] & kTileIdMask) != t) ranges[t].x = (uint32_t)e;
-  if (e == nd - 1 || (tile_key[e + 1] & kTileIdMask) != t) ranges[t].y = (uint32_t)(e + 1);
+  // four entries per thread: one 16 B key load, one 4 B mask store
+  const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (e0 >= nd) return;
+  uint32_t k[4];
+  if (e0 + 4 <= nd) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(tile_key) + (e0 >> 2));
+    k[0] = q.x; k[1] = q.y; k[2] = q.z; k[3] = q.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) k[j] = e0 + j < nd ? tile_key[e0 + j] : 0u;
+  }
+  uint32_t prev = e0 == 0 ? ~0u : (__ldg(tile_key + e0 - 1) & kTileIdMask);
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int64_t e = e0 + j;
+    if (e >= nd) break;
+    const uint32_t t = k[j] & kTileIdMask;
+    m |= (k[j] >> kMaskShift) << (8 * j);
+    if (t != prev) {
+      ranges[t].x = (uint32_t)e;
+      if (e > 0) ranges[prev].y = (uint32_t)e;
+    }
+    prev = t;
+  }
+  if (e0 + 4 >= nd) ranges[prev].y = (uint32_t)nd;  // the last entry closes its tile
+  if (e0 + 4 <= nd)
+    *reinterpret_cast<uint32_t*>(emask + e0) = m;
+  else
+    for (int j = 0; e0 + j < nd; ++j) emask[e0 + j] = (uint8_t)(m >> (8 * j));
 }
 
 // Blend work units (blend.cu): tile i of the longest-first order gets
@@ -565,7 +588,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
   f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
   f.emask.ensure(std::max<uint32_t>(nd, 1));
-  k_tile_ranges<<<blocks(nd, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get(),
+  k_tile_ranges<<<blocks((nd + 3) / 4, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get(),
                                                  f.emask.get());
   count_launch();
   {
