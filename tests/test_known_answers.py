@@ -1,0 +1,262 @@
+"""Known answers of the reference's own unit tests, re-hosted.
+
+Each test names the reference test it restates. The CPU half runs the
+oracle (and the reference compiled into oracle/_ref when present) against
+those known answers; the GPU half runs the same answers through the libdsg
+C ABI, at the GPU tolerances of test_gpu_parity.py where the reference's
+tolerance is an fp64 one.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import Oracle, Reference, has_reference
+from paper_2509_12138_b200.types import RenderConfig, SplatModel, TrainView
+from util import disc_mask, fd_scene, fp32_exact, full_mask, offset_ground_truth, random_scene
+from util import smooth_config
+from util import test_camera as make_camera
+
+IMPLS = ["oracle"] + (["reference"] if has_reference() else [])
+IMG_TOL = 1e-3  # device images (fp32) against fp64 answers, as test_gpu_parity.py
+
+
+@pytest.fixture(scope="module", params=IMPLS)
+def impl(request):
+    return Oracle() if request.param == "oracle" else Reference()
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2509_12138_b200 import api
+    return api.Context(0)
+
+
+def gaussian_row(mu, log_scale, opacity_logit, color, rot=(1.0, 0.0, 0.0, 0.0)):
+    return list(mu) + list(log_scale) + list(rot) + [opacity_logit] + list(color)
+
+
+def red_splat() -> SplatModel:
+    """test_rasterizer.cpp:65-73."""
+    return SplatModel(np.array([gaussian_row((0, 0, 0), (0, 0, 0), 12.0, (1, 0, 0))]))
+
+
+def stacked_pair() -> SplatModel:
+    """test_rasterizer.cpp:99-110: model order back-first, depth sort fixes it."""
+    ls = (math.log(0.2),) * 3
+    back = gaussian_row((0, 0, 0.5), ls, 0.0, (0, 0, 1))
+    front = gaussian_row((0, 0, -0.5), ls, 0.0, (1, 0, 0))
+    return SplatModel(np.array([back, front]))
+
+
+def opaque_triple() -> SplatModel:
+    """test_backward.cpp:75-91: two near-opaque front splats, one terminated away."""
+    ls = (math.log(0.4),) * 3
+    return SplatModel(np.array([gaussian_row((0, 0, -0.6), ls, 12.0, (1, 0, 0)),
+                                gaussian_row((0, 0, -0.2), ls, 12.0, (0, 1, 0)),
+                                gaussian_row((0, 0, 0.6), ls, 12.0, (0, 0, 1))]))
+
+
+def brute_force_pixel(proj, P, cfg: RenderConfig, x: int, y: int):
+    """composite_pixel_oracle (test_rasterizer.cpp:15-47): no tiles, no bins,
+    the compositing formula over (depth, index)-sorted projected splats."""
+    order = np.lexsort((proj["index"], proj["depth"]))
+    px, py = x + 0.5, y + 0.5
+    T = 1.0
+    acc = np.zeros(3)
+    for e in order:
+        i = proj["index"][e]
+        dx = px - proj["mean2d"][e, 0]
+        dy = py - proj["mean2d"][e, 1]
+        ixx, ixy, iyy = proj["inv_cov"][e]
+        q = ixx * dx * dx + 2 * ixy * dx * dy + iyy * dy * dy
+        if q > cfg.sigma_cutoff * cfg.sigma_cutoff:
+            continue
+        alpha = min(proj["opacity"][e] * math.exp(-0.5 * q), 0.999)
+        if alpha < cfg.alpha_cutoff:
+            continue
+        acc += P[i, 11:14] * (alpha * T)
+        T *= 1.0 - alpha
+        if T < cfg.transmittance_floor:
+            break
+    return acc + np.asarray(cfg.background) * T
+
+
+def mse_dl(out_color, target):
+    """test_backward.cpp:47-66: L = mean squared pixel error, dL/dpixel analytic."""
+    return 2.0 * (out_color - target) / out_color.size
+
+
+# --- CPU: the oracle (and the compiled reference) against the known answers --
+
+def test_empty_model_is_background(impl):
+    """test_rasterizer.cpp:51-63."""
+    out = impl.render(SplatModel(), make_camera(32), RenderConfig())
+    assert np.all(out.color == 1.0) and np.all(out.alpha == 0.0)
+
+
+def test_red_splat_covers_centre(impl):
+    """test_rasterizer.cpp:65-80."""
+    out = impl.render(red_splat(), make_camera(64), RenderConfig())
+    assert abs(out.color[32, 32, 0] - 1.0) <= 1 / 255
+    assert out.color[32, 32, 1] <= 1 / 255
+    assert out.alpha[32, 32] >= 0.99
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_brute_force_compositing(impl, seed):
+    """test_rasterizer.cpp:82-96: every third pixel within 1e-12."""
+    cfg, cam = RenderConfig(), make_camera(32)
+    model = random_scene(seed, 6)
+    out = impl.render(model, cam, cfg)
+    proj = impl.prepare(model, cam, cfg)
+    for y in range(0, 32, 3):
+        for x in range(0, 32, 3):
+            np.testing.assert_allclose(out.color[y, x], brute_force_pixel(proj, model.params, cfg, x, y),
+                                       rtol=1e-12, atol=0)
+
+
+def test_stacked_front_to_back(impl):
+    """test_rasterizer.cpp:98-119."""
+    cfg, cam, model = RenderConfig(), make_camera(64), stacked_pair()
+    out = impl.render(model, cam, cfg)
+    expect = brute_force_pixel(impl.prepare(model, cam, cfg), model.params, cfg, 32, 32)
+    np.testing.assert_allclose(out.color[32, 32], expect, rtol=1e-14, atol=0)
+    assert out.color[32, 32, 0] > out.color[32, 32, 2]
+
+
+def test_single_gaussian_mse_finite_differences(impl):
+    """test_backward.cpp:40-73: fd_scene(17, 1), target offset seed 99, h = 1e-4."""
+    cam, cfg = make_camera(32), smooth_config()
+    model = fd_scene(17, 1)
+    target = offset_ground_truth(impl.render, model, cam, cfg, 99)
+
+    def mse(m):
+        return float(np.mean((impl.render(m, cam, cfg).color - target) ** 2))
+
+    out = impl.render(model, cam, cfg)
+    g = impl.backward(model, cam, cfg, out, mse_dl(out.color, target)).grads
+    h = 1e-4
+    for p in range(14):
+        plus, minus = model.params.copy(), model.params.copy()
+        plus[0, p] += h
+        minus[0, p] -= h
+        fd = (mse(SplatModel(plus)) - mse(SplatModel(minus))) / (2 * h)
+        an = g[0, p]
+        assert abs(an - fd) <= max(1e-4 * max(abs(an), abs(fd)), 1e-8), (p, an, fd)
+
+
+def test_occluded_splat_gets_zero_gradient(impl):
+    """test_backward.cpp:75-107: T = (1 - 0.999)^2 < 1e-4 at the centre pixel."""
+    cam, cfg, model = make_camera(32), RenderConfig(), opaque_triple()
+    out = impl.render(model, cam, cfg)
+    dL = np.zeros((32, 32, 3))
+    dL[16, 16, :] = 1.0
+    g = impl.backward(model, cam, cfg, out, dL).grads
+    assert np.all(g[2, 11:14] == 0.0) and g[2, 10] == 0.0
+    assert np.linalg.norm(g[0, 11:14]) > 0.0
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+@pytest.mark.parametrize("lam", [0.0, 0.2])
+def test_loss_gradients_finite_differences(impl, seed, lam):
+    """test_backward.cpp:109-127 (check_loss_gradients, test_util.hpp:166-197)."""
+    cam, cfg = make_camera(32), smooth_config()
+    model = fd_scene(seed, 3)
+    view = TrainView(cam, offset_ground_truth(impl.render, model, cam, cfg, seed + 1000),
+                     full_mask(32, 32) if seed % 2 == 0 else disc_mask(32, 32, 14.0, 17.0, 11.0))
+
+    def loss(m):
+        return impl.masked_loss(impl.render(m, cam, cfg).color, view, lam).loss
+
+    out = impl.render(model, cam, cfg)
+    lr = impl.masked_loss(out.color, view, lam)
+    g = impl.backward(model, cam, cfg, out, lr.dL_dpixels).grads
+    h, floor, worst = 1e-4, 1e-8, 0.0
+    for gi in range(model.params.shape[0]):
+        for p in range(14):
+            plus, minus = model.params.copy(), model.params.copy()
+            plus[gi, p] += h
+            minus[gi, p] -= h
+            fd = (loss(SplatModel(plus)) - loss(SplatModel(minus))) / (2 * h)
+            err = abs(g[gi, p] - fd)
+            rel = 0.0 if err <= floor else err / max(abs(g[gi, p]), abs(fd), floor)
+            worst = max(worst, rel)
+    assert worst < 1e-4, worst
+
+
+def test_sharded_backward_bit_identical(impl):
+    """test_backward.cpp:129-157: shards 2, 4, 7 equal the unsharded pass exactly."""
+    cam, cfg = make_camera(32), RenderConfig()
+    model = random_scene(77, 6)
+    view = TrainView(cam, offset_ground_truth(impl.render, model, cam, cfg, 7), full_mask(32, 32))
+    out = impl.render(model, cam, cfg)
+    lr = impl.masked_loss(out.color, view, 0.2)
+    whole = impl.backward(model, cam, cfg, out, lr.dL_dpixels, 1)
+    for shards in (2, 4, 7):
+        part = impl.backward(model, cam, cfg, out, lr.dL_dpixels, shards)
+        np.testing.assert_array_equal(part.grads, whole.grads)
+        np.testing.assert_array_equal(part.d_mean2d, whole.d_mean2d)
+
+
+# --- GPU: the same known answers through the C ABI ---------------------------
+
+@pytest.mark.gpu
+def test_gpu_red_splat_covers_centre(ctx):
+    from paper_2509_12138_b200 import api
+    out = api.render(red_splat(), make_camera(64), RenderConfig(), ctx=ctx)
+    assert abs(out.color[32, 32, 0] - 1.0) <= 1 / 255
+    assert out.color[32, 32, 1] <= 1 / 255
+    assert out.alpha[32, 32] >= 0.99
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [21, 22, 23])
+def test_gpu_brute_force_compositing(ctx, seed):
+    from paper_2509_12138_b200 import api
+    cfg, cam = RenderConfig(), make_camera(32)
+    model = fp32_exact(random_scene(seed, 6))
+    out = api.render(model, cam, cfg, ctx=ctx)
+    proj = Oracle().prepare(model, cam, cfg)
+    for y in range(0, 32, 3):
+        for x in range(0, 32, 3):
+            expect = brute_force_pixel(proj, model.params, cfg, x, y)
+            assert np.max(np.abs(out.color[y, x] - expect)) <= IMG_TOL
+
+
+@pytest.mark.gpu
+def test_gpu_stacked_front_to_back(ctx):
+    from paper_2509_12138_b200 import api
+    cfg, cam, model = RenderConfig(), make_camera(64), fp32_exact(stacked_pair())
+    out = api.render(model, cam, cfg, ctx=ctx)
+    expect = brute_force_pixel(Oracle().prepare(model, cam, cfg), model.params, cfg, 32, 32)
+    assert np.max(np.abs(out.color[32, 32] - expect)) <= IMG_TOL
+    assert out.color[32, 32, 0] > out.color[32, 32, 2]
+    np.testing.assert_array_equal(out.splat_order, [1, 0])
+
+
+@pytest.mark.gpu
+def test_gpu_occluded_splat_gets_zero_gradient(ctx):
+    from paper_2509_12138_b200 import api
+    cam, cfg, model = make_camera(32), RenderConfig(), fp32_exact(opaque_triple())
+    out = api.render(model, cam, cfg, ctx=ctx)
+    dL = np.zeros((32, 32, 3))
+    dL[16, 16, :] = 1.0
+    g = api.backward(model, cam, cfg, out, dL, ctx=ctx).grads
+    assert np.all(g[2, 11:14] == 0.0) and g[2, 10] == 0.0
+    assert np.linalg.norm(g[0, 11:14]) > 0.0
+
+
+@pytest.mark.gpu
+def test_gpu_sharded_backward_bit_identical(ctx):
+    from paper_2509_12138_b200 import api
+    cam, cfg = make_camera(32), RenderConfig()
+    model = fp32_exact(random_scene(77, 6))
+    view = TrainView(cam, offset_ground_truth(Oracle().render, model, cam, cfg, 7), full_mask(32, 32))
+    out = api.render(model, cam, cfg, ctx=ctx)
+    lr = api.masked_loss(out.color, view, 0.2, ctx=ctx)
+    whole = api.backward(model, cam, cfg, out, lr.dL_dpixels, 1, ctx=ctx)
+    for shards in (2, 4, 7):
+        part = api.backward(model, cam, cfg, out, lr.dL_dpixels, shards, ctx=ctx)
+        np.testing.assert_array_equal(part.grads, whole.grads)
+        np.testing.assert_array_equal(part.d_mean2d, whole.d_mean2d)
