@@ -14,7 +14,7 @@ import pytest
 from oracle import Oracle, Reference, has_reference
 from paper_2509_12138_b200.types import RenderConfig, SplatModel, TrainView
 from util import disc_mask, fd_scene, fp32_exact, full_mask, offset_ground_truth, random_scene
-from util import smooth_config
+from util import Rng, smooth_config
 from util import test_camera as make_camera
 
 IMPLS = ["oracle"] + (["reference"] if has_reference() else [])
@@ -260,3 +260,164 @@ def test_gpu_sharded_backward_bit_identical(ctx):
         part = api.backward(model, cam, cfg, out, lr.dL_dpixels, shards, ctx=ctx)
         np.testing.assert_array_equal(part.grads, whole.grads)
         np.testing.assert_array_equal(part.d_mean2d, whole.d_mean2d)
+
+
+# --- projection, conservation, determinism, masks, rig -----------------------
+
+def test_projection_centre_depth_and_inverse_square(impl):
+    """test_gauss_core.cpp:75-101: target lands at (32, 32), depth 3; twice
+    the distance shrinks the undilated footprint trace 4x."""
+    cam, cfg = make_camera(64), RenderConfig()
+    ls = (math.log(0.1),) * 3
+    near = impl.prepare(SplatModel(np.array([gaussian_row((0, 0, 0), ls, 0.0, (1, 1, 1))])), cam, cfg)
+    assert abs(near["mean2d"][0, 0] - 32.0) < 0.5 and abs(near["mean2d"][0, 1] - 32.0) < 0.5
+    assert near["depth"][0] == pytest.approx(3.0)
+    far_mu = np.array(cam.position) + (np.zeros(3) - np.array(cam.position)) * 2.0
+    far = impl.prepare(SplatModel(np.array([gaussian_row(far_mu, ls, 0.0, (1, 1, 1))])), cam, cfg)
+
+    def trace(pr):
+        ixx, ixy, iyy = pr["inv_cov"][0]
+        det = ixx * iyy - ixy * ixy
+        return (ixx + iyy) / det - 2 * 0.3  # cov2d = inv(inv_cov); kCovDilation (projection.hpp:13)
+
+    assert trace(near) / trace(far) == pytest.approx(4.0, rel=0.01)
+
+
+def test_projection_spd_floor(impl):
+    """test_gauss_core.cpp:110-125: sub-pixel splats keep cov2d SPD with the 0.3 floor."""
+    rng = Rng(3)
+    P = []
+    for _ in range(50):
+        mu = (rng.uniform(-1, 1), rng.uniform(-1, 1), rng.uniform(-1, 1))
+        q = np.array([rng.normal() for _ in range(4)])
+        P.append(gaussian_row(mu, (math.log(1e-4),) * 3, 0.0, (1, 1, 1), tuple(q / np.linalg.norm(q))))
+    pr = impl.prepare(SplatModel(np.array(P)), make_camera(32), RenderConfig())
+    assert len(pr["index"]) == 50
+    ixx, ixy, iyy = pr["inv_cov"].T
+    det = ixx * iyy - ixy * ixy
+    assert np.all(det > 0)
+    assert np.all(iyy / det >= 0.3 - 1e-12) and np.all(ixx / det >= 0.3 - 1e-12)
+
+
+def test_projection_roll_equivariance(impl):
+    """test_gauss_core.cpp:127-151: rolling the camera by theta rotates mean2d by -theta."""
+    cam, cfg = make_camera(64), RenderConfig()
+    model = SplatModel(np.array([gaussian_row((0.4, 0.25, 0.1), (0, 0, 0), 0.0, (1, 1, 1))]))
+    base = impl.prepare(model, cam, cfg)["mean2d"][0]
+    th = 0.35
+    f = -np.array(cam.position) / np.linalg.norm(cam.position)
+    u = np.array(cam.up)
+    up = u * math.cos(th) + np.cross(f, u) * math.sin(th) + f * (f @ u) * (1 - math.cos(th))
+    rolled = make_camera(64)
+    rolled.up = tuple(up)
+    got = impl.prepare(model, rolled, cfg)["mean2d"][0]
+    d = base - 32.0
+    c, s = math.cos(-th), math.sin(-th)
+    np.testing.assert_allclose(got, [32 + c * d[0] - s * d[1], 32 + s * d[0] + c * d[1]], atol=1e-6)
+
+
+def conservation_check(render_fn, prepare_fn, tol_color, tol_alpha):
+    """test_rasterizer.cpp:136-187: sum(alpha_i T_i) + T_final = 1 per pixel,
+    the image equals the independent walk, alpha equals the weight sum."""
+    cam, cfg = make_camera(32), RenderConfig()
+    for seed in range(100, 110):
+        model = fp32_exact(random_scene(seed, 8))
+        out = render_fn(model, cam, cfg)
+        pr = prepare_fn(model, cam, cfg)
+        order = np.lexsort((pr["index"], pr["depth"]))
+        for y in range(32):
+            for x in range(32):
+                T, wsum, acc = 1.0, 0.0, np.zeros(3)
+                for e in order:
+                    dx, dy = x + 0.5 - pr["mean2d"][e, 0], y + 0.5 - pr["mean2d"][e, 1]
+                    ixx, ixy, iyy = pr["inv_cov"][e]
+                    q = ixx * dx * dx + 2 * ixy * dx * dy + iyy * dy * dy
+                    if q > cfg.sigma_cutoff ** 2:
+                        continue
+                    a = min(pr["opacity"][e] * math.exp(-0.5 * q), 0.999)
+                    if a < cfg.alpha_cutoff:
+                        continue
+                    wsum += a * T
+                    acc += model.params[pr["index"][e], 11:14] * (a * T)
+                    T *= 1.0 - a
+                    if T < cfg.transmittance_floor:
+                        break
+                assert abs(wsum + T - 1.0) < 1e-6
+                assert np.max(np.abs(out.color[y, x] - (acc + np.asarray(cfg.background) * T))) < tol_color
+                assert abs(out.alpha[y, x] - wsum) < tol_alpha
+
+
+def test_conservation(impl):
+    conservation_check(impl.render, impl.prepare, 1e-12, 1e-9)
+
+
+def mask_checks(mask_fn):
+    """test_rasterizer.cpp:200-249: empty, disc of radius ~4 at the centre,
+    union = OR of parts, footprint below half a pixel rejected."""
+    from paper_2509_12138_b200.types import DsplatError
+    assert np.all(mask_fn(np.zeros((0, 3)), make_camera(32), 2.0, 2.0) == 0.0)
+    m = mask_fn(np.zeros((1, 3)), make_camera(64), 2.0, 2.0)
+    ys, xs = np.mgrid[0:64, 0:64]
+    dist = np.hypot(xs + 0.5 - 32.0, ys + 0.5 - 32.0)
+    assert np.all(m[dist <= 3.0] == 1.0) and np.all(m[dist >= 5.0] == 0.0)
+    assert (dist <= 3.0).sum() <= (m == 1.0).sum() <= 3.15 * 25.0
+    rng = Rng(9)
+    cloud = np.array([[rng.uniform(-0.8, 0.8) for _ in range(3)] for _ in range(60)])
+    cam = make_camera(48)
+    full = mask_fn(cloud, cam, 2.0, 1.0)
+    np.testing.assert_array_equal(full, np.maximum(mask_fn(cloud[:25], cam, 2.0, 1.0),
+                                                   mask_fn(cloud[25:], cam, 2.0, 1.0)))
+    with pytest.raises(DsplatError):
+        mask_fn(np.zeros((1, 3)), make_camera(32), 0.2, 0.0)
+
+
+def test_mask_known_answers(impl):
+    mask_checks(impl.render_mask)
+
+
+def test_orbital_rig_counts(impl):
+    """test_gauss_core.cpp:153-183: 28x16 = 448 cameras; 1x1 is one +x camera;
+    every camera on the sphere; zero counts or radius rejected."""
+    from paper_2509_12138_b200.types import DsplatError
+    assert len(impl.build_orbital_cameras((0, 0, 0), 2.5, 28, 16, 64)) == 448
+    one = impl.build_orbital_cameras((1, 2, 3), 2.0, 1, 1, 64)
+    np.testing.assert_allclose(one[0].position, (3.0, 2.0, 3.0), atol=1e-12)
+    c = np.array([0.5, -1.0, 2.0])
+    rig = impl.build_orbital_cameras(c, 3.25, 7, 5, 32)
+    assert len(rig) == 35
+    for cam in rig:
+        assert abs(np.linalg.norm(np.array(cam.position) - c) - 3.25) < 1e-9
+        assert cam.target[0] == pytest.approx(0.5)
+    for args in ((1.0, 0, 4), (1.0, 4, 0), (0.0, 4, 4)):
+        with pytest.raises(DsplatError):
+            impl.build_orbital_cameras((0, 0, 0), args[0], args[1], args[2], 64)
+
+
+@pytest.mark.gpu
+def test_gpu_conservation(ctx):
+    from paper_2509_12138_b200 import api
+    conservation_check(lambda m, c, g: api.render(m, c, g, ctx=ctx), Oracle().prepare, IMG_TOL,
+                       IMG_TOL)
+
+
+@pytest.mark.gpu
+def test_gpu_determinism(ctx):
+    """test_rasterizer.cpp:189-198: repeat renders and backward passes are bit-identical."""
+    from paper_2509_12138_b200 import api
+    cam, cfg = make_camera(64), RenderConfig()
+    model = fp32_exact(random_scene(55, 40))
+    a = api.render(model, cam, cfg, ctx=ctx)
+    b = api.render(model, cam, cfg, ctx=ctx)
+    np.testing.assert_array_equal(a.color, b.color)
+    np.testing.assert_array_equal(a.alpha, b.alpha)
+    np.testing.assert_array_equal(a.splat_order, b.splat_order)
+    dL = np.random.default_rng(0).normal(size=(64, 64, 3))
+    ga = api.backward(model, cam, cfg, a, dL, ctx=ctx)
+    gb = api.backward(model, cam, cfg, b, dL, ctx=ctx)
+    np.testing.assert_array_equal(ga.grads, gb.grads)
+
+
+@pytest.mark.gpu
+def test_gpu_mask_known_answers(ctx):
+    from paper_2509_12138_b200 import api
+    mask_checks(lambda p, c, f, d: api.render_mask(p, c, f, d, ctx=ctx))
