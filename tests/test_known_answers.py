@@ -421,3 +421,56 @@ def test_gpu_determinism(ctx):
 def test_gpu_mask_known_answers(ctx):
     from paper_2509_12138_b200 import api
     mask_checks(lambda p, c, f, d: api.render_mask(p, c, f, d, ctx=ctx))
+
+
+# --- masked loss (test_trainer.cpp:12-96) -------------------------------------
+
+def loss_checks(loss_fn, render_fn, l1_tol, self_tol):
+    from paper_2509_12138_b200.types import DsplatError
+    cam = make_camera(32)
+    # identical images: zero loss and gradient (test_trainer.cpp:12-23)
+    img = np.array(render_fn(fp32_exact(random_scene(2, 3)), cam, RenderConfig()).color, np.float64)
+    lr = loss_fn(img, TrainView(cam, img.copy(), full_mask(32, 32)), 0.2)
+    assert abs(lr.loss) <= self_tol and np.all(np.abs(lr.dL_dpixels) < self_tol)
+    # all-zero mask is vacuous, exactly (test_trainer.cpp:25-36)
+    lr = loss_fn(np.full((32, 32, 3), 0.1), TrainView(cam, np.full((32, 32, 3), 0.9),
+                                                      np.zeros((32, 32))), 0.2)
+    assert lr.loss == 0.0 and np.all(lr.dL_dpixels == 0.0)
+    # lambda 0 is the elementwise L1 mean (test_trainer.cpp:38-54)
+    rng = Rng(4)
+    a = np.array([rng.uniform() for _ in range(16 * 16 * 3)]).reshape(16, 16, 3)
+    b = np.array([rng.uniform() for _ in range(16 * 16 * 3)]).reshape(16, 16, 3)
+    lr = loss_fn(a, TrainView(make_camera(16), b, full_mask(16, 16)), 0.0)
+    assert lr.loss == pytest.approx(np.mean(np.abs(a - b)), rel=l1_tol)
+    # dimension mismatch (test_trainer.cpp:56-65)
+    with pytest.raises(DsplatError, match="DimensionMismatch"):
+        loss_fn(np.zeros((32, 32, 3)), TrainView(cam, np.zeros((32, 32, 3)), np.zeros((16, 16))), 0.2)
+    # masked-out pixels are inert, bit-exact (test_trainer.cpp:67-96)
+    model, cfg = fp32_exact(random_scene(8, 3)), RenderConfig()
+    rendered = render_fn(model, cam, cfg).color
+    view = TrainView(cam, offset_ground_truth(Oracle().render, model, cam, cfg, 5),
+                     disc_mask(32, 32, 16, 16, 9.0))
+    base = loss_fn(rendered, view, 0.2)
+    poked_gt = view.ground_truth.copy()
+    rng = Rng(99)
+    for y in range(32):
+        for x in range(32):
+            if view.mask[y, x] < 0.5:
+                for c in range(3):
+                    poked_gt[y, x, c] = rng.uniform()
+    poked = loss_fn(rendered, TrainView(cam, poked_gt, view.mask), 0.2)
+    assert base.loss == poked.loss
+    np.testing.assert_array_equal(base.dL_dpixels, poked.dL_dpixels)
+    assert np.all(base.dL_dpixels[view.mask < 0.5] == 0.0)
+
+
+def test_loss_known_answers(impl):
+    loss_checks(impl.masked_loss, impl.render, 1e-12, 1e-12)
+
+
+@pytest.mark.gpu
+def test_gpu_loss_known_answers(ctx):
+    from paper_2509_12138_b200 import api
+    # device loss terms are fp32 images reduced in fp64
+    loss_checks(lambda r, v, lam: api.masked_loss(r, v, lam, ctx=ctx),
+                lambda m, c, g: api.render(m, c, g, ctx=ctx), 1e-6, 1e-6)
