@@ -474,3 +474,82 @@ def test_gpu_loss_known_answers(ctx):
     # device loss terms are fp32 images reduced in fp64
     loss_checks(lambda r, v, lam: api.masked_loss(r, v, lam, ctx=ctx),
                 lambda m, c, g: api.render(m, c, g, ctx=ctx), 1e-6, 1e-6)
+
+
+# --- partition and merge (test_partition.cpp:83-229) --------------------------
+
+def _impls_partition():
+    from paper_2509_12138_b200 import partition as part_mod
+    return [("host", part_mod.partition_cloud), ("oracle", Oracle().partition_cloud)]
+
+
+@pytest.mark.parametrize("which", [0, 1])
+def test_ghosts_within_margin_and_symmetric(which):
+    """test_partition.cpp:83-118."""
+    from paper_2509_12138_b200.types import owns
+    from util import random_cloud
+    pts = random_cloud(21, 400)
+    margin = 0.15
+    parts = _impls_partition()[which][1](pts, 3, margin)
+
+    def dist(p, v):
+        lo, hi = p.owned_box[0][p.cut_axis], p.owned_box[1][p.cut_axis]
+        return lo - v if v < lo else (v - hi if v > hi else 0.0)
+
+    for p in parts:
+        owned = set(p.owned_indices.tolist())
+        for gi in p.ghost_indices:
+            assert not owns(p, pts[gi])
+            assert dist(p, pts[gi][p.cut_axis]) <= margin
+            assert gi not in owned
+    for a in parts:
+        for i in a.owned_indices:
+            for b in parts:
+                if b.id != a.id and dist(b, pts[i][b.cut_axis]) <= margin:
+                    assert i in set(b.ghost_indices.tolist())
+
+
+def _model(mus, part, iteration=0):
+    P = np.zeros((len(mus), 14))
+    P[:, 0:3] = np.asarray(mus, dtype=np.float64).reshape(-1, 3)
+    P[:, 6] = 1.0
+    return SplatModel(P, iteration, part)
+
+
+def test_merge_drop_rules():
+    """test_partition.cpp:127-229: one partition is the identity (far
+    positions still owned); two partitions keep their own; foreign ghost
+    copies and splats that drifted across the cut are dropped."""
+    from paper_2509_12138_b200 import partition as part_mod
+    from util import random_cloud
+    orc = Oracle()
+
+    def both(models, parts):
+        merged = part_mod.merge_models(models, parts)
+        keep = orc.merge_keep([m.params for m in models], parts)
+        np.testing.assert_array_equal(merged.params,
+                                      np.concatenate([m.params for m in models])[keep])
+        return merged
+
+    parts = part_mod.partition_cloud(random_cloud(31, 50), 1, 0.1)
+    rng = Rng(5)
+    m = _model([[rng.uniform(-5, 5) for _ in range(3)] for _ in range(20)], 0, 7)
+    merged = both([m], parts)
+    np.testing.assert_array_equal(merged.params, m.params)
+    assert merged.iteration == 7
+
+    pts = np.array([[-0.5 - 0.01 * i if i < 10 else 0.5 + 0.01 * i, 0, 0] for i in range(20)])
+    parts = part_mod.partition_cloud(pts, 2, 0.05)
+    assert len(both([_model([[-0.5, 0, 0]], 0), _model([[0.5, 0, 0]], 1)], parts).params) == 2
+
+    pts = np.array([[-0.4 - 0.05 * i, 0, 0] for i in range(8)] + [[0.4 + 0.05 * i, 0, 0] for i in range(8)])
+    parts = part_mod.partition_cloud(pts, 2, 1.0)
+    assert len(parts[0].ghost_indices) > 0
+    m0 = _model(pts[np.concatenate([parts[0].owned_indices, parts[0].ghost_indices])], 0)
+    m1 = _model(pts[parts[1].owned_indices], 1)
+    assert len(both([m0, m1], parts).params) == len(pts)
+
+    pts = np.array([[-0.5 if i < 5 else 0.5, 0.01 * i, 0] for i in range(10)])
+    parts = part_mod.partition_cloud(pts, 2, 0.0)
+    merged = both([_model([[-0.5, 0, 0], [0.4, 0, 0]], 0), _model([[0.5, 0, 0]], 1)], parts)
+    assert merged.params[:, 0].tolist() == [-0.5, 0.5]
