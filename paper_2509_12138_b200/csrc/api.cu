@@ -7,6 +7,9 @@
 // reference so the C++ wrappers can rethrow identical dsplat::Error texts.
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -14,6 +17,9 @@
 #include <string>
 #include <thread>
 #include <vector>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -435,19 +441,94 @@ namespace {
 // through two pinned staging buffers, the DMA of one chunk overlapping a
 // multi-threaded host memcpy of the other (a single pageable cudaMemcpy is
 // bound by the driver's one-thread staging copy and first-touch faults).
+// Host worker pool for the staged copies: created once, reused by every
+// chunk (spawning 16 threads per 32 MiB chunk cost ~0.3 ms a chunk).
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  // fn(i) for i in [0, n) on the workers and the caller; returns when all are done
+  void run(int n, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> one(run_mu_);  // one job at a time
+    std::unique_lock<std::mutex> lk(mu_);
+    fn_ = &fn;
+    n_ = n;
+    next_ = 1;
+    pending_ = n - 1;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    fn(0);
+    lk.lock();
+    while (true) {  // the caller helps with items no worker has claimed yet
+      if (next_ >= n_) break;
+      const int i = next_++;
+      lk.unlock();
+      fn(i);
+      lk.lock();
+      --pending_;
+    }
+    done_.wait(lk, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    for (unsigned k = 1; k < std::min(hw, 16u); ++k)
+      workers_.emplace_back([this] { loop(); });
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(mu_);
+    while (true) {
+      cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+      if (stop_) return;
+      seen = gen_;
+      while (fn_ && next_ < n_) {
+        const int i = next_++;
+        const std::function<void(int)>* fn = fn_;
+        lk.unlock();
+        (*fn)(i);
+        lk.lock();
+        if (--pending_ == 0) done_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int n_ = 0, next_ = 0, pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 void par_memcpy(char* dst, const char* src, size_t n) {
   const size_t kMinPerThread = 1 << 20;
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t nt = std::min<size_t>({(size_t)std::min(hw, 16u), (n + kMinPerThread - 1) / kMinPerThread});
+  HostPool& pool = HostPool::get();
+  const size_t nt = std::min<size_t>((size_t)pool.size(), (n + kMinPerThread - 1) / kMinPerThread);
   if (nt <= 1) {
     std::memcpy(dst, src, n);
     return;
   }
   const size_t per = ((n + nt - 1) / nt + 4095) & ~size_t(4095);
-  std::vector<std::thread> th;
-  for (size_t o = 0; o < n; o += per)
-    th.emplace_back([=] { std::memcpy(dst + o, src + o, std::min(per, n - o)); });
-  for (auto& t : th) t.join();
+  pool.run((int)((n + per - 1) / per), [=](int k) {
+    const size_t o = (size_t)k * per;
+    std::memcpy(dst + o, src + o, std::min(per, n - o));
+  });
 }
 
 // Model parameters cross the bus as fp32 (what the device stores): the host
@@ -457,23 +538,50 @@ void par_memcpy(char* dst, const char* src, size_t n) {
 }  // namespace
 }  // extern "C"
 namespace {
+// Streaming (non-temporal) stores: the converted data is not read again by
+// this thread, and skipping the read-for-ownership of the destination cuts
+// host DRAM traffic by a third. Same rounding as the scalar cast (MXCSR
+// round-to-nearest, cvtpd2ps / cvtps2pd).
+inline void convert_span(double* dst, const float* src, size_t n) {
+  size_t i = 0;
+#if defined(__SSE2__)
+  for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) dst[i] = (double)src[i];
+  for (; i + 2 <= n; i += 2) {
+    const __m128 f = _mm_castpd_ps(_mm_load_sd(reinterpret_cast<const double*>(src + i)));
+    _mm_stream_pd(dst + i, _mm_cvtps_pd(f));
+  }
+  _mm_sfence();
+#endif
+  for (; i < n; ++i) dst[i] = (double)src[i];
+}
+inline void convert_span(float* dst, const double* src, size_t n) {
+  size_t i = 0;
+#if defined(__SSE2__)
+  for (; i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15); ++i) dst[i] = (float)src[i];
+  for (; i + 4 <= n; i += 4) {
+    const __m128 lo = _mm_cvtpd_ps(_mm_loadu_pd(src + i));
+    const __m128 hi = _mm_cvtpd_ps(_mm_loadu_pd(src + i + 2));
+    _mm_stream_ps(dst + i, _mm_movelh_ps(lo, hi));
+  }
+  _mm_sfence();
+#endif
+  for (; i < n; ++i) dst[i] = (float)src[i];
+}
+
 template <class H, class D>
 void par_convert(D* dst, const H* src, size_t n) {
   const size_t kMin = size_t(1) << 18;
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t nt = std::min<size_t>({(size_t)std::min(hw, 16u), (n + kMin - 1) / kMin});
+  HostPool& pool = HostPool::get();
+  const size_t nt = std::min<size_t>((size_t)pool.size(), (n + kMin - 1) / kMin);
   if (nt <= 1) {
-    for (size_t i = 0; i < n; ++i) dst[i] = (D)src[i];
+    convert_span(dst, src, n);
     return;
   }
-  const size_t per = (n + nt - 1) / nt;
-  std::vector<std::thread> th;
-  for (size_t o = 0; o < n; o += per)
-    th.emplace_back([=] {
-      const size_t e = std::min(n, o + per);
-      for (size_t i = o; i < e; ++i) dst[i] = (D)src[i];
-    });
-  for (auto& t : th) t.join();
+  const size_t per = (((n + nt - 1) / nt) + 15) & ~size_t(15);
+  pool.run((int)((n + per - 1) / per), [=](int k) {
+    const size_t o = (size_t)k * per;
+    convert_span(dst + o, src + o, std::min(per, n - o));
+  });
 }
 }  // namespace
 extern "C" {
