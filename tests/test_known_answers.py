@@ -641,3 +641,62 @@ def test_gpu_acceptance_c9_shards(ctx):
     for shards in (2, 4):
         np.testing.assert_array_equal(api.train_partition(init, views, cfg, shards, ctx=ctx).params,
                                       s1.params)
+
+
+# --- training (test_trainer.cpp: self-target descent, seed reproducibility) ----
+
+def self_target_check(render_fn, loss_fn, train_fn):
+    """'loss decreases an order of magnitude on a self-target': 200 steps in
+    four 50-step calls; final < initial / 10, each window <= 1.05x the last."""
+    from paper_2509_12138_b200.types import TrainConfig
+    cam, rcfg = make_camera(32), RenderConfig(background=(1.0, 1.0, 1.0))
+    target = fp32_exact(random_scene(13, 5))
+    gt = np.array(Oracle().render(target, cam, rcfg).color)
+    P = target.params.copy()
+    rng = Rng(14)
+    for i in range(P.shape[0]):
+        P[i, 0:3] += [rng.uniform(-0.05, 0.05) for _ in range(3)]
+        P[i, 11:14] = [min(max(P[i, 11 + c] + rng.uniform(-0.2, 0.2), 0.05), 0.95) for c in range(3)]
+    init = fp32_exact(SplatModel(P))
+    view = TrainView(cam, gt, full_mask(32, 32))
+    initial = loss_fn(render_fn(init, cam, rcfg).color, view, 0.2).loss
+    m, losses = init, []
+    for _ in range(4):
+        m = train_fn(m, [view], TrainConfig(iterations=50, densify_interval=0, render=rcfg, seed=3))
+        losses.append(loss_fn(render_fn(m, cam, rcfg).color, view, 0.2).loss)
+    assert losses[-1] < initial / 10.0, (initial, losses)
+    for a, b in zip(losses, losses[1:]):
+        assert b <= a * 1.05
+
+
+def reproducible_check(train_fn):
+    """'fixed seed is bit-reproducible': two 60-step runs (densify on) are equal."""
+    from paper_2509_12138_b200.types import TrainConfig
+    cam, rcfg = make_camera(32), RenderConfig()
+    init = fp32_exact(random_scene(33, 5))
+    view = TrainView(cam, np.array(Oracle().render(fp32_exact(random_scene(34, 5)), cam, rcfg).color),
+                     full_mask(32, 32))
+    cfg = TrainConfig(iterations=60, seed=77, render=rcfg)
+    np.testing.assert_array_equal(train_fn(init, [view], cfg).params, train_fn(init, [view], cfg).params)
+
+
+def test_self_target_descent(impl):
+    self_target_check(impl.render, impl.masked_loss, impl.train_partition)
+
+
+def test_fixed_seed_reproducible(impl):
+    reproducible_check(impl.train_partition)
+
+
+@pytest.mark.gpu
+def test_gpu_self_target_descent(ctx):
+    from paper_2509_12138_b200 import api
+    self_target_check(lambda m, c, g: api.render(m, c, g, ctx=ctx),
+                      lambda r, v, lam: api.masked_loss(r, v, lam, ctx=ctx),
+                      lambda m, vs, cfg: api.train_partition(m, vs, cfg, ctx=ctx))
+
+
+@pytest.mark.gpu
+def test_gpu_fixed_seed_reproducible(ctx):
+    from paper_2509_12138_b200 import api
+    reproducible_check(lambda m, vs, cfg: api.train_partition(m, vs, cfg, ctx=ctx))
