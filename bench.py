@@ -454,10 +454,11 @@ def run_ours(args, dist: Dist):
     e1 = time.perf_counter()
     api.train_device(dm_e, hv, train_config(args, dist.rank, args.steps))
     e2 = time.perf_counter()
+    e_dev_ms, _ = ctx.last_timing()  # the same loop's device span (events)
     out = dm_e.download()
     e_wall = time.perf_counter() - e0
     e_parts = {"upload_s": round(e1 - e0, 4), "train_s": round(e2 - e1, 4),
-               "download_s": round(e0 + e_wall - e2, 4)}
+               "download_s": round(e0 + e_wall - e2, 4), "train_device_s": round(e_dev_ms * 1e-3, 4)}
     e_max = dist.max(e_wall)
     view_bytes = npix * (3 * 4 + 1)
     # the model crosses the bus as fp32 (host converts from/to doubles)

@@ -1102,13 +1102,14 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
         blend_forward(f, m.params.get(), m.cap, cam, rd, st);
       }
       tm.mark(5, st);
-      masked_loss_dev(f, gt, mk, views->width, views->height, cfg->loss_lambda, st);
-      DSG_CUDA_CHECK(cudaMemcpyAsync(trace + it, f.loss_out.get(), sizeof(double),
-                                     cudaMemcpyDeviceToDevice, st));
-      if (views->host) {  // the step's result read back to the host; view slot free
+      masked_loss_dev(f, gt, mk, views->width, views->height, cfg->loss_lambda, st, trace + it);
+      if (views->host) {
+        // view slot free; the step's loss is read back on the copy stream, so
+        // the compute stream never queues behind the next view's H2D copy
         DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_consumed[slot], st));
-        DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->host_loss, f.loss_out.get(), sizeof(double),
-                                       cudaMemcpyDeviceToHost, st));
+        DSG_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[slot], 0));
+        DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->host_loss, trace + it, sizeof(double),
+                                       cudaMemcpyDeviceToHost, ctx->copy_stream));
       }
       tm.mark(6, st);
       if (!empty) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
@@ -1162,6 +1163,7 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     }
     DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_end, st));
     DSG_CUDA_CHECK(cudaEventSynchronize(ctx->ev_end));
+    if (views->host) DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->copy_stream));  // last loss read
     float total;
     DSG_CUDA_CHECK(cudaEventElapsedTime(&total, ctx->ev_begin, ctx->ev_end));
     ctx->last_total_ms = total;

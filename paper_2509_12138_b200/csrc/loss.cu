@@ -269,7 +269,7 @@ void ensure_window() {
 }  // namespace
 
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
-                     double lambda, cudaStream_t st) {
+                     double lambda, cudaStream_t st, double* out) {
   ensure_window();
   const int64_t npix = (int64_t)width * height;
   dim3 grid((width + kB - 1) / kB, (height + kB - 1) / kB);
@@ -292,7 +292,7 @@ void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, 
   a.parts = f.loss_parts.get();
   a.counts = f.loss_counts.get();
   a.dL = f.dL.get();
-  a.loss_out = f.loss_out.get();
+  a.loss_out = out ? out : f.loss_out.get();
   a.nblocks = nblocks;
   k_ssim_stats<<<grid, kB * kB, 0, st>>>(a);
   count_launch();

@@ -184,7 +184,7 @@ void blend_backward(Frame& f, const float* params, int64_t pitch, const CamDev& 
 void chain_3d(const ChainArgs& a, cudaStream_t st);
 void adam_update(const AdamArgs& a, cudaStream_t st);
 // Masked L1 + D-SSIM on f.rgb vs (gt, mask); writes f.dL and the loss into
-// f.loss_out[0] (device). gt planar fp32 [3][h*w], mask u8 [h*w].
+// `out` (default f.loss_out[0]; device). gt planar fp32 [3][h*w], mask u8 [h*w].
 // K11: stamp render_mask discs of `radius` px into a zeroed byte mask.
 void render_mask_dev(const double* pts, int64_t n, const CamDev& cam, double radius,
                      uint8_t* mask, cudaStream_t st);
@@ -231,6 +231,6 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& lo
 void gather_bands_dev(void* comm, int nranks, int rank, float* rgb, int width, int height,
                       const std::vector<int>& row0, const std::vector<int>& row1, cudaStream_t st);
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
-                     double lambda, cudaStream_t st);
+                     double lambda, cudaStream_t st, double* out = nullptr);
 
 }  // namespace dsg
