@@ -17,6 +17,7 @@
 #include <string>
 #include <thread>
 #include <vector>
+#include <unistd.h>
 #if defined(__SSE2__)
 #include <emmintrin.h>
 #endif
@@ -437,10 +438,6 @@ int dsg_model_destroy(dsg_model model) {
 
 namespace {
 
-// Copy between a large pageable host buffer and device memory: 32 MiB chunks
-// through two pinned staging buffers, the DMA of one chunk overlapping a
-// multi-threaded host memcpy of the other (a single pageable cudaMemcpy is
-// bound by the driver's one-thread staging copy and first-touch faults).
 // Host worker pool for the staged copies: created once, reused by every
 // chunk (spawning 16 threads per 32 MiB chunk cost ~0.3 ms a chunk).
 class HostPool {
@@ -452,6 +449,10 @@ class HostPool {
   int size() const { return (int)workers_.size() + 1; }
   // fn(i) for i in [0, n) on the workers and the caller; returns when all are done
   void run(int n, const std::function<void(int)>& fn) {
+    if (getpid() != pid_) {  // a forked child has no workers: run inline
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
     std::lock_guard<std::mutex> one(run_mu_);  // one job at a time
     std::unique_lock<std::mutex> lk(mu_);
     fn_ = &fn;
@@ -476,7 +477,7 @@ class HostPool {
   }
 
  private:
-  HostPool() {
+  HostPool() : pid_(getpid()) {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     for (unsigned k = 1; k < std::min(hw, 16u); ++k)
       workers_.emplace_back([this] { loop(); });
@@ -507,6 +508,7 @@ class HostPool {
       }
     }
   }
+  const pid_t pid_;
   std::vector<std::thread> workers_;
   std::mutex run_mu_, mu_;
   std::condition_variable cv_, done_;
@@ -516,6 +518,10 @@ class HostPool {
   bool stop_ = false;
 };
 
+// Copy between a large pageable host buffer and device memory: 32 MiB chunks
+// through two pinned staging buffers, the DMA of one chunk overlapping a
+// multi-threaded host memcpy of the other (a single pageable cudaMemcpy is
+// bound by the driver's one-thread staging copy and first-touch faults).
 void par_memcpy(char* dst, const char* src, size_t n) {
   const size_t kMinPerThread = 1 << 20;
   HostPool& pool = HostPool::get();

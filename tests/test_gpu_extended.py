@@ -256,3 +256,18 @@ def test_long_tile_lists_split(orc, ctx, opacity):
     ga = api.backward(model, cam, RenderConfig(), a, dl, ctx=ctx)
     gb = orc.backward(model, cam, RenderConfig(), b, dl)
     assert_grads_close(ga.grads, gb.grads)
+
+
+@pytest.mark.parametrize("n", [1, 37, 600_001])
+def test_model_transfer_round_trip(ctx, n):
+    """Staged host<->device model copies (pinned chunks, worker pool, streaming
+    stores): download(upload(P)) is P rounded to fp32, for ragged sizes that
+    leave unaligned tails and span several 32 MiB chunks."""
+    P = np.random.default_rng(n).normal(size=(n, 14)) * 10.0 ** np.random.default_rng(1).integers(-30, 30, size=(n, 14))
+    dm = api.DeviceModel(ctx, SplatModel(P, 5, 2))
+    out = dm.download()
+    np.testing.assert_array_equal(out.params, P.astype(np.float32).astype(np.float64))
+    assert out.iteration == 5 and out.origin_partition == 2
+    dm.upload(SplatModel(P[: max(1, n // 2)]))
+    np.testing.assert_array_equal(dm.download().params,
+                                  P[: max(1, n // 2)].astype(np.float32).astype(np.float64))
