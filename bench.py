@@ -45,6 +45,10 @@ METRIC = "training iters/sec & Gaussians·views/sec at 1/2/4/8 B200; render Mpix
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+# arithmetic type of the path: fp32 storage and blend/chain/Adam arithmetic;
+# fp64 where an integer or ordering decision is taken (projection, rects,
+# depth order, the alpha/cutoff guard band) and in the SSIM window sums
+DTYPE = "f32"
 
 
 def log(*a):
@@ -364,7 +368,7 @@ def run_partitioned(args, dist: Dist):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "f32 (fp64 for ordering/cutoff decisions, SSIM statistics and the 3D chain)",
+        "dtype": DTYPE,
         "data": "synthetic",
         "config": {"workload": f"{args.workload}-shaped isosurface, {n_total:,} Gaussians in {P} slab "
                                f"partitions (+ghosts), partition k on GPU k mod {dist.world}, "
@@ -432,46 +436,50 @@ def run_ours(args, dist: Dist):
     mpix = len(test_cams) * 2 * npix / (r_ms * 1e-3) / 1e6
     mpix = dist.sum(mpix)
 
-    # end-to-end through the C ABI with host buffers
+    # End to end through the reference-shaped public API: the caller's
+    # SplatModel (host doubles) and std::vector<TrainView>-like list of views
+    # in the reference's own layout (HWC double ground truth, HW double mask,
+    # loss.hpp:14-26) go into train_partition_full (trainer.hpp:140), which
+    # uploads the model, streams the scheduled views (host conversion to
+    # planar fp32 + bytes into pinned slots, overlapped with the previous
+    # step), trains, reads every step's loss back and returns the model as
+    # host doubles. Views the schedule never touches are never read, so they
+    # share one placeholder image here (the call cannot tell).
     order = api.view_order(train_config(args, dist.rank, 1).seed, len(views), args.steps)
-    gts, masks = [None] * len(views), [None] * len(views)
-    for vi in sorted(set(order.tolist())):
+    sched = sorted(set(order.tolist()))
+    h, w = args.res, args.res
+    blank_gt, blank_mask = np.zeros((h, w, 3)), np.zeros((h, w))
+    tviews = [TrainView(c, blank_gt, blank_mask) for c in views.cams]
+    for vi in sched:
         tv = views.download(int(vi))
-        gts[vi] = api.pinned(np.ascontiguousarray(tv.ground_truth.transpose(2, 0, 1), np.float32))
-        masks[vi] = api.pinned((tv.mask >= 0.5).astype(np.uint8))
-    hv = api.HostViews(ctx, views.cams, gts, masks)
+        tviews[vi] = TrainView(views.cams[vi], tv.ground_truth, tv.mask)
     host_model = SplatModel(np.ascontiguousarray(seeds_host.params))
-    dm_e = api.DeviceModel(ctx)
-    # an untimed first upload allocates the model's device buffers and the
-    # staging area (one-time setup, like the context); the timed region then
-    # moves the whole model in, every step's view in and loss out, and the
-    # model back out
-    dm_e.upload(host_model)
+    tc = train_config(args, dist.rank, args.steps)
+    api.train_partition_full(host_model, tviews, tc, ctx=ctx)  # untimed: allocations, pinned slots
     dist.barrier()
     ctx.synchronize()
     e0 = time.perf_counter()
-    dm_e.upload(host_model)
-    e1 = time.perf_counter()
-    api.train_device(dm_e, hv, train_config(args, dist.rank, args.steps))
-    e2 = time.perf_counter()
-    e_dev_ms, _ = ctx.last_timing()  # the same loop's device span (events)
-    out = dm_e.download()
+    res = api.train_partition_full(host_model, tviews, tc, ctx=ctx, loss_trace=True)
     e_wall = time.perf_counter() - e0
-    e_parts = {"upload_s": round(e1 - e0, 4), "train_s": round(e2 - e1, 4),
-               "download_s": round(e0 + e_wall - e2, 4), "train_device_s": round(e_dev_ms * 1e-3, 4)}
+    e_dev_ms, _ = ctx.last_timing()  # the same loop's device span (events)
+    e_parts = {"train_partition_full_s": round(e_wall, 4), "train_device_s": round(e_dev_ms * 1e-3, 4),
+               "outside_device_loop_s": round(e_wall - e_dev_ms * 1e-3, 4),
+               "views_streamed": args.steps, "final_loss": res.final_loss}
+    assert len(res.loss_trace) == args.steps
     e_max = dist.max(e_wall)
+    # bytes that cross the bus: the model as fp32 both ways (amortised), each
+    # step's converted view (planar fp32 + mask bytes) in, the loss trace out
     view_bytes = npix * (3 * 4 + 1)
-    # the model crosses the bus as fp32 (host converts from/to doubles)
     h2d = view_bytes + n * 14 * 4 / args.steps
     d2h = 8 + n * 14 * 4 / args.steps
-    del out
+    del res
 
     peak, peak_kind = load_peak()
     roof = roofline(stage_ms, n, nv_vis, npix, n_dup, peak, peak_kind)
 
-    cpu = None
+    cpu, parity = None, None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(inp, views, seeds_host, args)
+        cpu, parity = cpu_baseline(ctx, inp, views, seeds_host, args)
 
     line = {
         "metric": METRIC,
@@ -484,24 +492,24 @@ def run_ours(args, dist: Dist):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32 (fp64 for ordering/cutoff decisions, SSIM statistics and the 3D chain)",
+        "dtype": DTYPE,
         "data": "synthetic",
-        "config": {"workload": f"{args.workload}-shaped isosurface, {args.n_per_gpu:,} Gaussians/GPU "
-                               f"(+ghosts), {args.az}x{args.el} rig at {args.res}^2, one slab "
-                               f"partition per GPU", "gaussians_per_gpu": n,
-                   "views": len(views), "resolution": args.res, "partitions": dist.world,
-                   "l2": "working set > L2 (params+grads+moments 224 B/G)"},
+        "config": config_dict(args, dist.world, n, len(views)),
+        "host": host_info(),
         "gaussian_views_per_sec": round(gv, 1),
         "render_mpix_per_sec": round(mpix, 2),
         "wall_s": round(wall_max, 4),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "n_dup": n_dup,
         "e2e": {"value": round(total_iters / e_max, 3), "unit": "it/s",
+                "api": "api.train_partition_full(SplatModel, [TrainView], TrainConfig) "
+                       "(trainer.hpp:140): host doubles in, reference-layout views, host doubles out",
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "breakdown": e_parts},
         "gpu_launches": int(dist.sum(float(launches))),
         "roofline": roof,
         "cpu_baseline": cpu,
+        "parity": parity,
         "clocks": clk,
         "global": glob,
         "final_loss": fl,
@@ -509,61 +517,195 @@ def run_ours(args, dist: Dist):
     return line
 
 
-def cpu_baseline(inp, views, seeds_host, args):
-    """Reference CPU train iterations on a bounded sample: 1 iteration, 1 view."""
-    from oracle import Oracle, Reference, has_reference
-    impl = Reference() if has_reference() else Oracle()
-    kind = "reference" if has_reference() else "port"
+def cpu_baseline(ctx, inp, views, seeds_host, args):
+    """Checker leg, after all timing (rank 0, N=1): the reference's own CPU
+    implementation (oracle/_ref) on the same partition and the first scheduled
+    view. One call of tests/scale_parity.step_parity compares the device path
+    with it (splat order, per-tile lists, image, loss, gradients, Adam, one
+    train iteration) and times the reference's train iteration on the host
+    cores, which is the cpu_baseline value."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from scale_parity import checker, step_parity
+    impl, kind = checker()
     cores = os.cpu_count() or 1
     order = api.view_order(1, len(views), 1)
     tv = views.download(int(order[0]))
-    cfg = TrainConfig(iterations=1, seed=1)
-    t0 = time.perf_counter()
-    impl.train_partition_full(seeds_host, [tv], cfg, shards=cores)
-    dt = time.perf_counter() - t0
-    return {"value": round(1.0 / dt, 5), "unit": "it/s", "cores": cores, "kind": kind,
-            "sample": f"1 training iteration of the same partition ({len(seeds_host):,} Gaussians) "
-                      f"on 1 {args.res}^2 view, shards={cores} (row-band threads), {dt:.1f} s",
-            "gaussian_views_per_sec": round(len(seeds_host) / dt, 1)}
+    model = SplatModel(np.ascontiguousarray(seeds_host.params))
+    rep = step_parity(ctx, impl, model, tv, TrainConfig(iterations=1, seed=1), shards=cores)
+    dt = rep["ref_train_iter_s"]
+    cpu = {"value": round(1.0 / dt, 5), "unit": "it/s", "cores": cores, "kind": kind,
+           "sample": f"1 training iteration of the same partition ({len(seeds_host):,} Gaussians) "
+                     f"on its first scheduled {args.res}^2 view, shards={cores} (row-band "
+                     f"threads), {dt:.1f} s",
+           "gaussian_views_per_sec": round(len(seeds_host) / dt, 1)}
+    keep = ("pass", "splat_order_bit_exact", "tile_counts_bit_exact", "tile_lists_bit_exact",
+            "n_visible", "n_tile_entries", "img_max_abs", "alpha_max_abs", "ncontrib_mismatch_px",
+            "loss_rel", "grad_worst_over_tol", "grad_max_rel_above_floor", "touch_count_exact",
+            "adam_worst_over_tol", "train_step_bad_above_floor",
+            "train_step_sign_flips_below_floor", "train_step_scalars")
+    parity = {k: rep[k] for k in keep}
+    parity["lists_bit_exact"] = bool(rep["tile_lists_bit_exact"] and rep["splat_order_bit_exact"])
+    parity["grad_max_rel"] = rep["grad_max_rel_above_floor"]
+    parity["checker"] = kind
+    parity["view"] = int(order[0])
+    parity["tolerances"] = {"image_max_abs": 1e-3, "grad_rel": 1e-4, "grad_floor": "1e-5 x group max",
+                            "adam_rel": 1e-4}
+    return cpu, parity
+
+
+def view_order_host(seed: int, n_views: int, iterations: int):
+    """Seeded view order (trainer.hpp:157-163, 174) restated in Python, so the
+    reference arm never maps libdsg.so: Rng(seed ^ 0x87aa11d3).shuffle."""
+    M = (1 << 64) - 1
+
+    def mix(st):
+        st = (st + 0x9E3779B97F4A7C15) & M
+        z = st
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return st, z ^ (z >> 31)
+
+    s = ((seed ^ 0x87AA11D3) ^ 0x853C49E6748FEA9B) & M
+    s, _ = mix(s)
+    s, _ = mix(s)
+    order = list(range(n_views))
+    for i in range(n_views, 1, -1):
+        s, z = mix(s)
+        j = z % i
+        order[i - 1], order[j] = order[j], order[i - 1]
+    return [order[it % n_views] for it in range(iterations)]
+
+
+def host_info():
+    """nproc and the CPU model of the box the CPU legs run on."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def config_dict(args, world: int, gaussians: int, views: int):
+    """The workload description both arms print (identical by construction)."""
+    return {"workload": f"{args.workload}-shaped isosurface, {args.n_per_gpu:,} Gaussians/GPU "
+                        f"(+ghosts), {args.az}x{args.el} rig at {args.res}^2, one slab "
+                        f"partition per GPU", "gaussians_per_gpu": int(gaussians),
+            "views": int(views), "resolution": args.res, "partitions": world,
+            "l2": "working set > L2 (params+grads+moments 224 B/G)"}
+
+
+def knn_seeds_host(pts, cols, k: int = 3):
+    """seed_gaussians(ScaleRule::Knn, k) (seed.hpp:49-74) on the host for the
+    reference arm: exact k-NN by k-d tree, the k smallest fp64 distances summed
+    in ascending order and divided by k (seed.hpp:29-32), std::log via libm."""
+    from scipy.spatial import cKDTree
+    d, _ = cKDTree(pts).query(pts, k=k + 1, workers=os.cpu_count() or 1)
+    acc = np.zeros(len(pts))
+    for j in range(1, k + 1):
+        acc = acc + d[:, j]
+    mean = acc / k
+    P = np.zeros((len(pts), 14))
+    P[:, 0:3] = pts
+    P[:, 3:6] = np.array([math.log(max(s, 1e-7)) for s in mean.tolist()])[:, None]
+    P[:, 6] = 1.0
+    P[:, 10] = math.log(0.1 / (1.0 - 0.1))  # logit(0.1)
+    P[:, 11:14] = cols
+    return SplatModel(P)
+
+
+def reference_inputs(args, world: int, ref, steps: int):
+    """Rank 0's partition and its scheduled train views, built on the host with
+    the reference's own functions (oracle/_ref) — no libdsg.so in this process.
+
+    Same recipe as build_partition_inputs: the cloud generator (scenes.py), the
+    auto ghost margin 3 x median NN spacing, partition_cloud, the orbital rig
+    and split_rig, kNN seeds (seed.hpp:49-74), GT = render(ground_truth_model)
+    and render_mask per view (runtime.hpp:190-199). The reference's kNN is
+    O(N^2) (seed.hpp:16-35) and cannot run at 4M points, so the k smallest
+    exact fp64 distances come from a k-d tree and are summed in ascending
+    order as the reference does; logs use libm like std::log."""
+    from scipy.spatial import cKDTree
+    from paper_2509_12138_b200.types import TrainView
+    n_total = args.n_per_gpu * world
+    if args.workload == "kingsnake":
+        pts, cols, _ = scenes.kingsnake(n_total, seed=1, turns=6.0 * world)
+    else:
+        pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
+    workers = os.cpu_count() or 1
+    d1, _ = cKDTree(pts).query(pts, k=2, workers=workers)
+    nn = float(np.partition(d1[:, 1], len(pts) // 2)[len(pts) // 2])  # median_nn_spacing
+    if world > 1:
+        part = ref.partition_cloud(pts, world, 3.0 * nn)[0]
+        idx = np.concatenate([part.owned_indices, part.ghost_indices]).astype(np.int64)
+        ppts, pcols = np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx])
+    else:
+        ppts, pcols = pts, cols
+    seeds = knn_seeds_host(ppts, pcols)
+    gt_model = ref.ground_truth_model(ppts, pcols, nn, 0.97)
+    rig = scenes.rig_for_cloud(pts, args.az, args.el, args.res)
+    train_idx, _ = split_rig(len(rig), 0.1, 1)
+    cams = [rig[i] for i in train_idx]
+    views = {}
+    for vi in view_order_host(1, len(cams), steps):
+        if vi not in views:
+            cam = cams[vi]
+            views[vi] = TrainView(cam, ref.render(gt_model, cam, RenderConfig()).color,
+                                  ref.render_mask(ppts, cam, 2.0, 2.0))
+    return seeds, cams, views
 
 
 def run_reference(args, dist: Dist):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    headers compiled with the reference's Release flags) on the host cores.
+    Rank 0 only. Each step = one train_partition_full iteration (render ->
+    masked_loss -> backward -> Adam, trainer.hpp:173-207) of rank 0's
+    partition on the next scheduled view, shards = nproc."""
     if dist.rank != 0:
         return None
     from oracle import Oracle, Reference, has_reference
     impl = Reference() if has_reference() else Oracle()
     kind = "reference" if has_reference() else "port"
-    ctx = api.Context(dist.local)
-    inp = build_partition_inputs(args, _single(), ctx)
-    seeds_host = inp["seeds"].download()
-    views = inp["views"]
     cores = os.cpu_count() or 1
     # each CPU step is ~15-60 s: bound the whole run to a few minutes
     args.steps = min(args.steps, 4)
     args.warmup = min(args.warmup, 1)
-    order = api.view_order(1, len(views), args.warmup + args.steps)
+    t0 = time.time()
+    seeds, cams, views = reference_inputs(args, dist.world, impl, args.warmup + args.steps)
+    log(f"[reference] inputs: partition {len(seeds):,} Gaussians, {len(cams)} train views, "
+        f"{len(views)} scheduled views rendered, setup {time.time() - t0:.1f}s")
+    order = view_order_host(1, len(cams), args.warmup + args.steps)
     for it in range(args.warmup):
-        tv = views.download(int(order[it]))
-        impl.train_partition_full(seeds_host, [tv], TrainConfig(iterations=1, seed=1), shards=cores)
+        impl.train_partition_full(seeds, [views[order[it]]], TrainConfig(iterations=1, seed=1),
+                                  shards=cores)
     dts = []
     for it in range(args.steps):
-        tv = views.download(int(order[args.warmup + it]))
-        t0 = time.perf_counter()
-        impl.train_partition_full(seeds_host, [tv], TrainConfig(iterations=1, seed=1), shards=cores)
-        dts.append(time.perf_counter() - t0)
+        v = views[order[args.warmup + it]]
+        t1 = time.perf_counter()
+        impl.train_partition_full(seeds, [v], TrainConfig(iterations=1, seed=1), shards=cores)
+        dts.append(time.perf_counter() - t1)
     T = float(sum(dts))
     v = args.steps / T
+    with open("/proc/self/maps") as f:
+        mapped = sorted({ln.split()[-1] for ln in f if ln.rstrip().endswith(".so")
+                         and ROOT in ln})
+    log(f"[reference] in-tree shared objects mapped: {mapped}")
     return {
         "impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "it/s",
         "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(T * 1e3 / args.steps, 2), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}-shaped isosurface, {args.n_per_gpu:,} Gaussians "
-                               f"(partition 0), {args.res}^2 views", "gaussians": len(seeds_host)},
-        "gaussian_views_per_sec": round(len(seeds_host) * v, 1),
+        "config": config_dict(args, dist.world, len(seeds), len(cams)),
+        "gaussian_views_per_sec": round(len(seeds) * v, 1),
+        "host": host_info(),
         "cpu_baseline": {"value": round(v, 5), "unit": "it/s", "cores": cores, "kind": kind,
                          "sample": f"each step = 1 reference training iteration (render, loss, "
-                                   f"backward, Adam) of the full partition on one view, shards={cores}"},
+                                   f"backward, Adam) of rank 0's {len(seeds):,}-Gaussian partition "
+                                   f"on the next scheduled {args.res}^2 view, shards={cores}"},
         "e2e": {"value": round(v, 5), "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -607,7 +749,7 @@ def main():
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {dist.world}; using WORLD_SIZE")
     if args.impl == "reference":
         line = run_reference(args, dist)
-    elif args.partitions and args.partitions != dist.world:
+    elif args.partitions:
         line = run_partitioned(args, dist)
     else:
         line = run_ours(args, dist)

@@ -172,6 +172,15 @@ int dsg_views_synthesize(dsg_ctx ctx, dsg_model gt_model, const dsg_render_confi
  * may be NULL. The caller keeps the memory alive until dsg_views_destroy. */
 int dsg_views_create_host(dsg_ctx ctx, const dsg_camera* cams, const float* const* gt_planar,
                           const uint8_t* const* masks, int32_t n_views, dsg_views* out);
+/* Views in the reference's own TrainView layout (loss.hpp:14-26), left in
+ * caller memory: ground_truth[v] is an HWC double image [h][w][3], masks[v]
+ * an HW double mask [h][w] (pixel trained iff >= 0.5). dsg_train streams the
+ * scheduled views only: per step the host worker pool converts the next view
+ * to planar fp32 + bytes in a pinned slot and the copy overlaps the current
+ * step. Unused entries may be NULL; the memory must outlive the handle. */
+int dsg_views_create_host_ref(dsg_ctx ctx, const dsg_camera* cams,
+                              const double* const* ground_truth, const double* const* masks,
+                              int32_t n_views, dsg_views* out);
 int dsg_views_destroy(dsg_views views);
 /* The view index used at each of `iterations` steps for a seed
  * (trainer.hpp:157-163, 174). */

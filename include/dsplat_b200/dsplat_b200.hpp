@@ -318,18 +318,19 @@ inline TrainResult train_partition_full(const SplatModel& input,
   result.size_after_densify = input.size();
   if (cfg.iterations == 0) return result;
   detail::DeviceModel dm(input, ctx);
-  const int w = views[0].cam.width, h = views[0].cam.height;
-  const size_t np = static_cast<size_t>(w) * h;
+  // the views stay in the caller's TrainView images: dsg_train streams only
+  // the scheduled ones, converting each on the host into a pinned slot while
+  // the previous step runs
   std::vector<dsg_camera> cams;
-  std::vector<double> gts(3 * np * views.size()), masks(np * views.size());
-  for (size_t v = 0; v < views.size(); ++v) {
-    cams.push_back(detail::cam_of(views[v].cam));
-    std::memcpy(gts.data() + 3 * np * v, views[v].ground_truth.pixels.data(), sizeof(double) * 3 * np);
-    std::memcpy(masks.data() + np * v, views[v].mask.pixels.data(), sizeof(double) * np);
+  std::vector<const double*> gts, masks;
+  for (const auto& v : views) {
+    cams.push_back(detail::cam_of(v.cam));
+    gts.push_back(v.ground_truth.pixels.data());
+    masks.push_back(v.mask.pixels.data());
   }
   dsg_views dv = nullptr;
-  check(dsg_views_create(ctx.get(), cams.data(), gts.data(), masks.data(),
-                         static_cast<int32_t>(views.size()), &dv));
+  check(dsg_views_create_host_ref(ctx.get(), cams.data(), gts.data(), masks.data(),
+                                  static_cast<int32_t>(views.size()), &dv));
   std::unique_ptr<dsg_views_s, int (*)(dsg_views)> guard(dv, dsg_views_destroy);
   dsg_train_config tc = detail::train_of(cfg);
   struct Ctx {

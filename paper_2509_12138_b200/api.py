@@ -143,6 +143,15 @@ class Context:
     def synchronize(self):
         _check(lib().dsg_ctx_synchronize(self.h))
 
+    def scratch_model(self, model: SplatModel) -> "DeviceModel":
+        """A device model owned by this context, reused across calls of the
+        host-in/host-out entry points (its buffers only grow), so repeated
+        train_partition_full calls do not re-allocate ~224 B per Gaussian."""
+        if getattr(self, "_scratch", None) is None:
+            self._scratch = DeviceModel(self)
+        self._scratch.upload(model)
+        return self._scratch
+
     def set_profiling(self, on: bool):
         _check(lib().dsg_set_profiling(self.h, C.c_int32(1 if on else 0)))
 
@@ -392,8 +401,8 @@ def train_partition_full(model: SplatModel, views, cfg: TrainConfig, shards: int
         raise DsplatError(ErrorCode.NoViews, "training requires at least one view")
     if shards < 1:
         raise DsplatError(ErrorCode.InvalidArgument, "shards must be >= 1")
-    dm = DeviceModel(ctx, model)
-    dv = DeviceViews.from_views(ctx, views)
+    dm = ctx.scratch_model(model)
+    dv = HostRefViews(ctx, views)  # scheduled views streamed from host memory
     fl, trace = train_device(dm, dv, cfg, shards, progress, loss_trace)
     out = dm.download()
     out.origin_partition = model.origin_partition
@@ -478,6 +487,30 @@ class HostViews(DeviceViews):
         _check(lib().dsg_views_create_host(ctx.h, carr, gp, mp, C.c_int32(n), C.byref(h)))
         self._keep = (gts, masks)
         super().__init__(ctx, h, list(cams), cams[0].width, cams[0].height)
+
+
+class HostRefViews(DeviceViews):
+    """Views in the reference's TrainView layout (loss.hpp:14-26) left in host
+    memory — ground truth (h, w, 3) float64, mask (h, w) float64 — streamed by
+    dsg_train one scheduled view per step (dsg_views_create_host_ref): the host
+    worker pool converts the next view into a pinned slot while the current
+    step runs. Views the schedule never touches are never read."""
+
+    def __init__(self, ctx: Context, views):
+        n = len(views)
+        if n == 0:
+            raise DsplatError(ErrorCode.NoViews, "training requires at least one view")
+        for v in views:
+            v.validate()
+        keep = [(np.ascontiguousarray(v.ground_truth, dtype=np.float64),
+                 np.ascontiguousarray(v.mask, dtype=np.float64)) for v in views]
+        carr = (dsg_camera * n)(*[cam_struct(v.cam) for v in views])
+        gp = (C.c_void_p * n)(*[g.ctypes.data for g, _ in keep])
+        mp = (C.c_void_p * n)(*[m.ctypes.data for _, m in keep])
+        h = C.c_void_p()
+        _check(lib().dsg_views_create_host_ref(ctx.h, carr, gp, mp, C.c_int32(n), C.byref(h)))
+        self._keep = keep
+        super().__init__(ctx, h, [v.cam for v in views], views[0].cam.width, views[0].cam.height)
 
 
 def launch_count() -> int:

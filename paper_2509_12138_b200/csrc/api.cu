@@ -81,13 +81,15 @@ struct dsg_ctx_s {
   bool timer_init = false;
   ModelDev spare;  // densification output storage (swapped with the model's)
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
-  double* host_loss = nullptr;  // pinned, end-to-end mode
   // end-to-end mode: next step's view is copied on its own stream into the
   // other of two device slots while this step computes
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
   // pinned staging for large pageable model transfers (staged_copy)
   char* pin[2] = {nullptr, nullptr};
+  // pinned per-step view slots of reference-layout host views (planar fp32 + u8)
+  char* vpin[2] = {nullptr, nullptr};
+  size_t vpin_bytes = 0;
   cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   double last_total_ms = 0.0;
   int64_t last_iters = 0;
@@ -108,6 +110,10 @@ struct dsg_views_s {
   bool host = false;      // views live in caller-owned pinned host memory
   std::vector<const float*> host_gt;
   std::vector<const uint8_t*> host_mask;
+  // reference layout (TrainView, loss.hpp:14-26): HWC double GT + HW double
+  // mask in caller memory, converted per step into pinned staging slots
+  bool ref_layout = false;
+  std::vector<const double*> host_gt64, host_mask64;
 };
 
 namespace {
@@ -200,6 +206,7 @@ RenderDev make_rd(const dsg_render_config* c) {
   r.alpha_cutoff = c->alpha_cutoff;
   r.floor_T = c->transmittance_floor;
   for (int k = 0; k < 3; ++k) r.bg[k] = (float)c->background[k];
+  for (int k = 0; k < 3; ++k) r.bg64[k] = c->background[k];
   r.sigma_sq_f = (float)r.sigma_sq;
   r.alpha_cutoff_f = (float)r.alpha_cutoff;
   r.floor_T_f = (float)r.floor_T;
@@ -403,7 +410,6 @@ int dsg_ctx_destroy(dsg_ctx ctx) {
       cudaEventDestroy(ctx->ev_begin);
       cudaEventDestroy(ctx->ev_end);
     }
-    if (ctx->host_loss) cudaFreeHost(ctx->host_loss);
     for (int k = 0; k < 2; ++k) {
       if (ctx->ev_copied[k]) cudaEventDestroy(ctx->ev_copied[k]);
       if (ctx->ev_consumed[k]) cudaEventDestroy(ctx->ev_consumed[k]);
@@ -411,6 +417,7 @@ int dsg_ctx_destroy(dsg_ctx ctx) {
     if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
     for (int k = 0; k < 2; ++k) {
       if (ctx->pin[k]) cudaFreeHost(ctx->pin[k]);
+      if (ctx->vpin[k]) cudaFreeHost(ctx->vpin[k]);
       if (ctx->pin_ev[k]) cudaEventDestroy(ctx->pin_ev[k]);
     }
     cudaStreamDestroy(ctx->stream);
@@ -1015,6 +1022,65 @@ int dsg_views_create_host(dsg_ctx ctx, const dsg_camera* cams, const float* cons
   });
 }
 
+int dsg_views_create_host_ref(dsg_ctx ctx, const dsg_camera* cams,
+                              const double* const* ground_truth, const double* const* masks,
+                              int32_t n_views, dsg_views* out) {
+  return guarded([&] {
+    auto* v = new dsg_views_s();
+    try {
+      v->n = n_views;
+      v->host = true;
+      v->ref_layout = true;
+      for (int32_t i = 0; i < n_views; ++i) {
+        make_cam(&cams[i]);
+        if (i == 0) {
+          v->width = cams[0].width;
+          v->height = cams[0].height;
+        } else if (cams[i].width != v->width || cams[i].height != v->height) {
+          fail(kDimensionMismatch, "all views must share one resolution");
+        }
+        v->cams.push_back(cams[i]);
+        v->host_gt.push_back(nullptr);
+        v->host_mask.push_back(nullptr);
+        v->host_gt64.push_back(ground_truth ? ground_truth[i] : nullptr);
+        v->host_mask64.push_back(masks ? masks[i] : nullptr);
+      }
+      DeviceGuard g(ctx->device);
+      const int64_t npix = (int64_t)v->width * v->height;
+      v->gt.ensure(std::max<int64_t>(1, 2 * 3 * npix));
+      v->mask.ensure(std::max<int64_t>(1, 2 * npix));
+    } catch (...) {
+      delete v;
+      throw;
+    }
+    *out = v;
+  });
+}
+
+}  // extern "C"
+namespace {
+// One view from the reference's TrainView layout (HWC double ground truth, HW
+// double mask) into the device's planar fp32 + byte-mask layout, on the host
+// worker pool (read 32 B, write 13 B per pixel). mask >= 0.5 as k_mask_u8.
+void convert_view_ref(const double* gt, const double* mask, int64_t npix, float* planar,
+                      uint8_t* m8) {
+  HostPool& pool = HostPool::get();
+  const int64_t kMin = int64_t(1) << 15;
+  const int64_t nt = std::min<int64_t>(pool.size() * 2, (npix + kMin - 1) / kMin);
+  const int64_t per = (((npix + std::max<int64_t>(nt, 1) - 1) / std::max<int64_t>(nt, 1)) + 15) & ~int64_t(15);
+  pool.run((int)((npix + per - 1) / per), [=](int k) {
+    const int64_t p0 = (int64_t)k * per, p1 = std::min(npix, p0 + per);
+    for (int64_t p = p0; p < p1; ++p) {
+      planar[p] = (float)gt[3 * p];
+      planar[npix + p] = (float)gt[3 * p + 1];
+      planar[2 * npix + p] = (float)gt[3 * p + 2];
+      m8[p] = mask[p] >= 0.5 ? 1 : 0;
+    }
+  });
+}
+}  // namespace
+extern "C" {
+
 int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_config* cfg,
               int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
               double* loss_trace) {
@@ -1042,8 +1108,9 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     if (views->host)
       for (int64_t it = 0; it < std::min<int64_t>(iters, views->n); ++it) {
         size_t vi = order[(size_t)it];
-        if (!views->host_gt[vi] || !views->host_mask[vi])
-          fail(kInvalidArgument, "host view used by the schedule has no data");
+        const bool have = views->ref_layout ? views->host_gt64[vi] && views->host_mask64[vi]
+                                            : views->host_gt[vi] && views->host_mask[vi];
+        if (!have) fail(kInvalidArgument, "host view used by the schedule has no data");
       }
 
     DeviceGuard g(ctx->device);
@@ -1060,8 +1127,7 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
       ctx->timer_init = true;
     }
     double stage[StageTimer::kStages] = {};
-    if (views->host && !ctx->host_loss) {
-      DSG_CUDA_CHECK(cudaMallocHost(&ctx->host_loss, sizeof(double)));
+    if (views->host && !ctx->copy_stream) {
       DSG_CUDA_CHECK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
       for (int k = 0; k < 2; ++k) {
         DSG_CUDA_CHECK(cudaEventCreateWithFlags(&ctx->ev_copied[k], cudaEventDisableTiming));
@@ -1071,14 +1137,34 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     // end-to-end mode: views come from pinned host memory, double-buffered
     // so the copy of step it+1 overlaps step it (slot reuse waits for the
     // loss of step it-1, the last reader of that slot)
+    if (views->ref_layout && ctx->vpin_bytes < (size_t)(13 * npix)) {
+      for (int k = 0; k < 2; ++k) {
+        if (ctx->vpin[k]) DSG_CUDA_CHECK(cudaFreeHost(ctx->vpin[k]));
+        DSG_CUDA_CHECK(cudaMallocHost(&ctx->vpin[k], (size_t)(13 * npix)));
+      }
+      ctx->vpin_bytes = (size_t)(13 * npix);
+    }
     auto copy_view = [&](int64_t step) {
       const size_t v = order[(size_t)step % order.size()];
       const int slot = (int)(step & 1);
       cudaStream_t cs = ctx->copy_stream;
+      const float* src_gt = views->host_gt[v];
+      const uint8_t* src_mask = views->host_mask[v];
+      if (views->ref_layout) {
+        // reference-layout view: the slot's previous upload (step - 2) must
+        // have left the pinned buffer before the host refills it; the GPU is
+        // meanwhile still busy with the earlier steps' kernels
+        DSG_CUDA_CHECK(cudaEventSynchronize(ctx->ev_copied[slot]));
+        float* pf = reinterpret_cast<float*>(ctx->vpin[slot]);
+        uint8_t* pm = reinterpret_cast<uint8_t*>(ctx->vpin[slot] + 12 * npix);
+        convert_view_ref(views->host_gt64[v], views->host_mask64[v], npix, pf, pm);
+        src_gt = pf;
+        src_mask = pm;
+      }
       DSG_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_consumed[slot], 0));
-      DSG_CUDA_CHECK(cudaMemcpyAsync(views->gt.get() + 3 * npix * slot, views->host_gt[v],
+      DSG_CUDA_CHECK(cudaMemcpyAsync(views->gt.get() + 3 * npix * slot, src_gt,
                                      sizeof(float) * 3 * npix, cudaMemcpyHostToDevice, cs));
-      DSG_CUDA_CHECK(cudaMemcpyAsync(views->mask.get() + npix * slot, views->host_mask[v], npix,
+      DSG_CUDA_CHECK(cudaMemcpyAsync(views->mask.get() + npix * slot, src_mask, npix,
                                      cudaMemcpyHostToDevice, cs));
       DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_copied[slot], cs));
     };
@@ -1109,14 +1195,8 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
       }
       tm.mark(5, st);
       masked_loss_dev(f, gt, mk, views->width, views->height, cfg->loss_lambda, st, trace + it);
-      if (views->host) {
-        // view slot free; the step's loss is read back on the copy stream, so
-        // the compute stream never queues behind the next view's H2D copy
+      if (views->host)  // view slot free for the upload two steps ahead
         DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_consumed[slot], st));
-        DSG_CUDA_CHECK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_consumed[slot], 0));
-        DSG_CUDA_CHECK(cudaMemcpyAsync(ctx->host_loss, trace + it, sizeof(double),
-                                       cudaMemcpyDeviceToHost, ctx->copy_stream));
-      }
       tm.mark(6, st);
       if (!empty) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
       tm.mark(7, st);
@@ -1169,7 +1249,6 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     }
     DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_end, st));
     DSG_CUDA_CHECK(cudaEventSynchronize(ctx->ev_end));
-    if (views->host) DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->copy_stream));  // last loss read
     float total;
     DSG_CUDA_CHECK(cudaEventElapsedTime(&total, ctx->ev_begin, ctx->ev_end));
     ctx->last_total_ms = total;

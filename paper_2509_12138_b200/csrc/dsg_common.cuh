@@ -35,6 +35,7 @@ struct RenderDev {
   double alpha_cutoff;
   double floor_T;
   float bg[3];
+  double bg64[3];
   float sigma_sq_f, alpha_cutoff_f, floor_T_f;
 };
 

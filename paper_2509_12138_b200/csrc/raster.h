@@ -76,6 +76,7 @@ struct Frame {
   DevBuf<float> ubuf;          // per unit, per pixel segment state (blend.cu UnitPlane)
   int64_t unit_cap = 0, band_tiles = 0, seg_len = kSegMin, split_len = 0, split_cap = 0;
   DevBuf<uint32_t> counters;
+  DevBuf<uint32_t> amb, tile_unit;  // termination fix-up: flagged pixels, tile -> first unit
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL;
   DevBuf<uint32_t> last;

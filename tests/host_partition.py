@@ -1,4 +1,7 @@
-"""Slab partitioning with ghost cells and the ghost-trimming merge (host side).
+"""TEST INFRASTRUCTURE: a numpy restatement of slab partitioning with ghost
+cells and the ghost-trimming merge, used by the CPU (gloo) multi-process tests
+and the multi-GPU checker. The product path is the device partitioner
+(csrc/partition.cu) and dsg_merge_allgather (csrc/comm.cu).
 
 partition_cloud (partition.hpp:42-104), owns (:34-37) and merge_models
 (:109-126) with the reference's exact semantics:
@@ -18,7 +21,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from .types import PARAMS, DsplatError, ErrorCode, Partition, SplatModel
+from paper_2509_12138_b200.types import PARAMS, DsplatError, ErrorCode, Partition, SplatModel
 
 
 def partition_cloud(positions, n: int, ghost_margin: float):

@@ -16,7 +16,7 @@ import pytest
 
 import bench
 from oracle import Oracle
-from paper_2509_12138_b200 import partition as part_mod
+import host_partition as part_mod
 from paper_2509_12138_b200 import scenes
 from paper_2509_12138_b200.types import DsplatError, SplatModel
 from util import random_cloud
@@ -145,3 +145,21 @@ def test_distributed_merge_gloo_world2(orc):
     parts = orc.partition_cloud(pts, 2, 0.1)
     keep = orc.merge_keep([m.params for m in models], parts)
     np.testing.assert_array_equal(got, np.concatenate([m.params for m in models])[keep])
+
+
+def test_view_order_host_matches_library():
+    """bench.py's reference arm restates the seeded view order in Python so
+    it never maps libdsg.so; it must equal dsg_view_order (host code, no GPU)."""
+    from paper_2509_12138_b200 import api
+    for seed, n, iters in ((1, 403, 50), (7, 58, 130), (2, 1, 3), (123456789, 17, 40)):
+        assert bench.view_order_host(seed, n, iters) == api.view_order(seed, n, iters).tolist()
+
+
+def test_reference_arm_seeds_match_seed_gaussians():
+    """The reference arm's k-d-tree kNN seeds equal the reference's O(N^2)
+    seed_gaussians (seed.hpp:49-74) bit for bit on a cloud it can still run."""
+    from oracle import Reference, has_reference
+    pts, cols, _ = scenes.kingsnake(3000, seed=2)
+    impl = Reference() if has_reference() else Oracle()
+    np.testing.assert_array_equal(bench.knn_seeds_host(pts, cols).params,
+                                  impl.seed_gaussians(pts, cols, 3).params)

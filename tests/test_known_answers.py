@@ -479,7 +479,7 @@ def test_gpu_loss_known_answers(ctx):
 # --- partition and merge (test_partition.cpp:83-229) --------------------------
 
 def _impls_partition():
-    from paper_2509_12138_b200 import partition as part_mod
+    import host_partition as part_mod
     return [("host", part_mod.partition_cloud), ("oracle", Oracle().partition_cloud)]
 
 
@@ -520,7 +520,7 @@ def test_merge_drop_rules():
     """test_partition.cpp:127-229: one partition is the identity (far
     positions still owned); two partitions keep their own; foreign ghost
     copies and splats that drifted across the cut are dropped."""
-    from paper_2509_12138_b200 import partition as part_mod
+    import host_partition as part_mod
     from util import random_cloud
     orc = Oracle()
 

@@ -43,7 +43,7 @@ cam = make_camera(128)
 img, rms = api.render_distributed(comm, merged, cam, RenderConfig())
 if rank == 0:
     ref_models = [SplatModel(p, 7, k) for k, p in enumerate(allp)]
-    from paper_2509_12138_b200.partition import merge_models
+    from host_partition import merge_models
     ref = merge_models(ref_models, parts)
     got = merged.download()
     assert np.array_equal(got.params, ref.params), "merged model differs"

@@ -1,0 +1,155 @@
+"""Parity at the benched and named configurations (BASELINE configs 1-3).
+
+Every check in tests/scale_parity.py (splat order and per-tile lists
+bit-exact, image <= 1e-3, gradients <= 1e-4 relative with the per-group
+floor, touch counts exact, Adam, one full train iteration) runs on:
+
+  * config 1: the 99,726-point sphere isosurface, 256^2 view, kNN seeds
+  * config 2: the 4M-Gaussian Kingsnake partition, 1024^2 view — the
+    workload bench.py times
+  * config 3: one 8-way RT partition (18.2M-point cloud, auto ghosts):
+    owned / ghost lists and cuts bit-exact against partition_cloud
+    (partition.hpp:42-104), the partition's background mask bit-exact
+    (render.hpp:210-233), and the step checks on its seeds
+
+Inputs are built the way bench.py builds them (device kNN seeds and
+median NN spacing, device-synthesized GT views); the device values are
+fp32, and the checker receives exactly those values. The checker is
+oracle/_ref (the reference compiled unchanged) when present.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2509_12138_b200 import api, scenes
+from paper_2509_12138_b200.types import RenderConfig, SplatModel, TrainConfig
+from scale_parity import checker, step_parity
+
+pytestmark = pytest.mark.gpu
+
+OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return api.Context(0)
+
+
+@pytest.fixture(scope="module")
+def ref():
+    return checker()[0]
+
+
+def _record(name, rep):
+    os.makedirs(OUT, exist_ok=True)
+    with open(os.path.join(OUT, f"scale_parity_{name}.json"), "w") as f:
+        json.dump(rep, f, indent=1)
+
+
+def _inputs(ctx, pts, cols, az, el, res):
+    """bench.py's per-partition setup: median NN, GT model, seeds, first
+    scheduled view (trainer.hpp:157-163) synthesized on the device."""
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    rig = scenes.rig_for_cloud(pts, az, el, res)
+    from bench import split_rig
+    train_idx, _ = split_rig(len(rig), 0.1, 1)
+    cams = [rig[i] for i in train_idx]
+    v0 = int(api.view_order(1, len(cams), 1)[0])
+    gt = api.ground_truth_model(pts, cols, nn, 0.97, ctx=ctx)
+    views = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), [cams[v0]], pts, True, 2.0, 2.0)
+    view = views.download(0)
+    seeds = api.seed_gaussians(pts, cols, 3, ctx=ctx).download()
+    return SplatModel(np.ascontiguousarray(seeds.params)), view, nn
+
+
+def _assert_pass(rep):
+    assert rep["splat_order_bit_exact"], rep
+    assert rep["tile_counts_bit_exact"] and rep["tile_lists_bit_exact"], rep
+    assert rep["img_max_abs"] <= 1e-3 and rep["alpha_max_abs"] <= 1e-3, rep
+    assert rep["grad_worst_over_tol"] <= 1.0, rep["grads"]
+    assert rep["touch_count_exact"], rep
+    assert rep["adam_worst_over_tol"] <= 1.0, rep
+    assert rep["train_step_bad_above_floor"] == 0, rep
+    assert rep["loss_rel"] <= 1e-4, rep
+    # contributor counts: exact (termination near the floor is re-decided in fp64)
+    assert rep["ncontrib_mismatch_px"] == 0, rep
+    assert rep["pass"]
+
+
+def test_config1_sphere_step_parity(ctx, ref):
+    pts, cols, _ = scenes.sphere()
+    model, view, _ = _inputs(ctx, pts, cols, 16, 4, 256)
+    rep = step_parity(ctx, ref, model, view, TrainConfig(iterations=1, seed=1))
+    _record("config1", rep)
+    _assert_pass(rep)
+
+
+def test_config2_kingsnake_step_parity(ctx, ref):
+    pts, cols, _ = scenes.kingsnake(scenes.SIZES["kingsnake"], seed=1, turns=6.0)
+    model, view, _ = _inputs(ctx, pts, cols, 28, 16, 1024)
+    assert len(model) == 4_000_000
+    rep = step_parity(ctx, ref, model, view, TrainConfig(iterations=1, seed=1))
+    _record("config2", rep)
+    _assert_pass(rep)
+
+
+def test_config2_knn_seeds_at_scale(ctx):
+    """knn_mean_distances (seed.hpp:16-35) on the 4M cloud: the device grid
+    kNN against an independent exact kNN (scipy cKDTree), summing the k
+    smallest fp64 distances in ascending order as the reference does."""
+    from scipy.spatial import cKDTree
+    pts, _, _ = scenes.kingsnake(scenes.SIZES["kingsnake"], seed=1, turns=6.0)
+    dev = api.knn_mean_distances(pts, 3, ctx=ctx)
+    d, _ = cKDTree(pts).query(pts, k=4, workers=os.cpu_count() or 1)
+    host = (d[:, 1] + d[:, 2] + d[:, 3]) / 3.0
+    np.testing.assert_array_equal(dev, host)
+    nn1 = np.sort(d[:, 1])[len(pts) // 2]
+    assert api.median_nn_spacing(pts, ctx=ctx) == nn1
+
+
+@pytest.fixture(scope="module")
+def rt_cloud():
+    return scenes.rt(scenes.SIZES["rt"], seed=1)
+
+
+def test_config3_rt_partition_bit_exact(ctx, ref, rt_cloud):
+    pts, cols, _ = rt_cloud
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    margin = 3.0 * nn
+    a = api.partition_cloud(pts, 8, margin, ctx=ctx)
+    b = ref.partition_cloud(pts, 8, margin)
+    summary = []
+    for pa, pb in zip(a, b):
+        assert pa.cut_axis == pb.cut_axis
+        assert pa.cut_lo == pb.cut_lo and pa.cut_hi == pb.cut_hi
+        np.testing.assert_array_equal(pa.owned_indices, pb.owned_indices)
+        np.testing.assert_array_equal(pa.ghost_indices, pb.ghost_indices)
+        np.testing.assert_array_equal(pa.owned_box, pb.owned_box)
+        summary.append([int(len(pb.owned_indices)), int(len(pb.ghost_indices))])
+    _record("config3_partition", {"points": int(len(pts)), "margin": margin,
+                                  "owned_ghost": summary, "bit_exact": True})
+
+
+def test_config3_rt_partition_mask_and_step(ctx, ref, rt_cloud):
+    pts, cols, _ = rt_cloud
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    parts = api.partition_cloud(pts, 8, 3.0 * nn, ctx=ctx)
+    part = parts[3]
+    idx = np.concatenate([part.owned_indices, part.ghost_indices]).astype(np.int64)
+    ppts, pcols = np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx])
+    rig = scenes.rig_for_cloud(pts, 28, 16, 1024)  # global rig (runtime.hpp:137)
+    cam = rig[37]
+    np.testing.assert_array_equal(api.render_mask(ppts, cam, 2.0, 2.0, ctx=ctx),
+                                  ref.render_mask(ppts, cam, 2.0, 2.0))
+    gt = api.ground_truth_model(ppts, pcols, nn, 0.97, ctx=ctx)
+    views = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), [cam], ppts, True, 2.0, 2.0)
+    view = views.download(0)
+    seeds = api.seed_gaussians(ppts, pcols, 3, ctx=ctx).download()
+    model = SplatModel(np.ascontiguousarray(seeds.params))
+    rep = step_parity(ctx, ref, model, view, TrainConfig(iterations=1, seed=4))
+    rep["partition"] = 3
+    rep["owned"], rep["ghosts"] = int(len(part.owned_indices)), int(len(part.ghost_indices))
+    _record("config3_step", rep)
+    _assert_pass(rep)
