@@ -463,6 +463,7 @@ def run_ours(args, dist: Dist):
     e_wall = time.perf_counter() - e0
     e_dev_ms, _ = ctx.last_timing()  # the same loop's device span (events)
     e_parts = {"train_partition_full_s": round(e_wall, 4), "train_device_s": round(e_dev_ms * 1e-3, 4),
+               **{k: round(v, 4) for k, v in getattr(ctx, "last_phases", {}).items()},
                "outside_device_loop_s": round(e_wall - e_dev_ms * 1e-3, 4),
                "views_streamed": args.steps, "final_loss": res.final_loss}
     assert len(res.loss_trace) == args.steps

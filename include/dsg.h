@@ -104,6 +104,12 @@ int dsg_model_info(dsg_model model, int64_t* n, int64_t* iteration, int64_t* ada
  * order, adam.hpp:104-112) and the step counter. */
 int dsg_model_adam_state(dsg_ctx ctx, dsg_model model, double* m, double* v, int64_t* step);
 
+/* Set the Adam moments (same layout as dsg_model_adam_state; NULL = zeros)
+ * and step counter of a device model holding n Gaussians — AdamState::resize
+ * / remap (adam.hpp:26-49) and checkpoint resume on the drop-in side. */
+int dsg_model_adam_restore(dsg_ctx ctx, dsg_model model, const double* m, const double* v,
+                           int64_t n, int64_t step);
+
 /* ---- render path ---------------------------------------------------------- */
 /* render (render.hpp:160-205). Outputs (each may be NULL): rgb [h][w][3],
  * alpha [h][w], n_contrib [h][w], splat_order (capacity n) and its length,
@@ -197,6 +203,16 @@ int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t v, double* ground_t
 int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_config* cfg,
               int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
               double* loss_trace);
+/* CheckpointSink (trainer.hpp:119-120): called on the host thread every
+ * checkpoint_interval steps and once at the end (trainer.hpp:204-209) with
+ * the model's iteration and the step's loss; the stream is idle, so the
+ * callback may read `model` with dsg_model_download / dsg_model_adam_state. */
+typedef void (*dsg_checkpoint_fn)(int64_t iteration, double loss, dsg_model model, void* user);
+/* dsg_train with a checkpoint callback (NULL = none). */
+int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
+                           const dsg_train_config* cfg, int32_t shards, dsg_progress_fn progress,
+                           void* user, dsg_checkpoint_fn checkpoint, void* ckpt_user,
+                           double* final_loss, double* loss_trace);
 
 /* ---- partition / merge / multi-GPU (partition.hpp) --------------- */
 /* partition_cloud (partition.hpp:42-104) on the device: positions [n][3];

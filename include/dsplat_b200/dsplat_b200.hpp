@@ -244,11 +244,13 @@ inline GradientBuffer backward(const SplatModel& model, const Camera& cam, const
 }
 
 // AdamState (adam.hpp:19-119): moments live on the device with a private
-// device copy of the model being optimised.
+// device copy of the model being optimised. resize / remap / serialize keep
+// the reference's semantics: moments set on the host (remap gathers them,
+// resize zeroes them) are installed on the device before the next step.
 class AdamState {
  public:
   static constexpr int kScalars = 14;
-  explicit AdamState(size_t n = 0) : n_(n) {}
+  explicit AdamState(size_t n = 0) { resize(n); }
   ~AdamState() {
     if (h_) dsg_model_destroy(h_);
   }
@@ -258,17 +260,65 @@ class AdamState {
   int64_t step_count() const { return step_; }
   using GroupRates = dsplat::AdamState::GroupRates;
 
+  // adam.hpp:26-29: n zeroed moments (the step count is kept)
+  void resize(size_t n) {
+    n_ = n;
+    pm_.assign(n * kScalars, 0.0);
+    pv_.assign(n * kScalars, 0.0);
+    pending_ = true;
+  }
+
+  // adam.hpp:36-49: entry j inherits the moments of source[j] (-1 = fresh)
+  void remap(const std::vector<int32_t>& source) {
+    std::vector<double> m, v;
+    moments(m, v);
+    std::vector<double> nm(source.size() * kScalars, 0.0), nv(source.size() * kScalars, 0.0);
+    for (size_t j = 0; j < source.size(); ++j) {
+      if (source[j] < 0) continue;
+      const size_t src = static_cast<size_t>(source[j]);
+      std::copy_n(m.begin() + src * kScalars, kScalars, nm.begin() + j * kScalars);
+      std::copy_n(v.begin() + src * kScalars, kScalars, nv.begin() + j * kScalars);
+    }
+    n_ = source.size();
+    pm_ = std::move(nm);
+    pv_ = std::move(nv);
+    pending_ = true;
+  }
+
+  // adam.hpp:103-112: [step, size, m..., v...]
+  std::vector<double> serialize() const {
+    std::vector<double> m, v;
+    moments(m, v);
+    std::vector<double> out;
+    out.reserve(2 + m.size() + v.size());
+    out.push_back(static_cast<double>(step_));
+    out.push_back(static_cast<double>(n_));
+    out.insert(out.end(), m.begin(), m.end());
+    out.insert(out.end(), v.begin(), v.end());
+    return out;
+  }
+
+  // adam.hpp:55-101. Parameters whose device update is zero (no gradient
+  // yet) keep their exact fp64 value; updated ones come back as the device
+  // computed them (fp32).
   void step(SplatModel& model, const GradientBuffer& grads, const GroupRates& lr,
             const AdamConfig& cfg = {}) {
     Context& ctx = Context::current();
     auto p = detail::params_of(model);
     const int64_t n = static_cast<int64_t>(model.size());
-    if (!h_) {
-      check(dsg_model_create(ctx.get(), &h_));
+    if (model.size() != n_) resize(model.size());
+    if (!h_) check(dsg_model_create(ctx.get(), &h_));
+    if (dev_n_ != n) {
       check(dsg_model_upload(ctx.get(), h_, p.data(), n, model.iteration, -1));
-      n_ = model.size();
+      dev_n_ = n;
+      pending_ = true;  // upload zeroed the device moments
     } else {
       check(dsg_model_set_params(ctx.get(), h_, p.data(), n, model.iteration));
+    }
+    if (pending_) {
+      check(dsg_model_adam_restore(ctx.get(), h_, pm_.empty() ? nullptr : pm_.data(),
+                                   pv_.empty() ? nullptr : pv_.data(), n, step_));
+      pending_ = false;
     }
     std::vector<double> g(14 * model.size());
     for (size_t i = 0; i < model.size(); ++i) {
@@ -284,22 +334,57 @@ class AdamState {
     dsg_adam_config a{cfg.beta1, cfg.beta2, cfg.epsilon};
     check(dsg_adam_step(ctx.get(), h_, g.data(), &r, &a));
     ++step_;
+    std::vector<double> out(p.size());
     int64_t nn = 0, it = 0;
     int32_t op = -1;
-    check(dsg_model_download(ctx.get(), h_, p.data(), static_cast<int64_t>(p.size() / 14), &nn,
-                             &it, &op));
+    check(dsg_model_download(ctx.get(), h_, out.data(), n, &nn, &it, &op));
+    for (size_t k = 0; k < p.size(); ++k)
+      if (out[k] != static_cast<double>(static_cast<float>(p[k]))) p[k] = out[k];
     detail::params_to(p, model);
   }
 
+  // A host-only snapshot (checkpoints): moments and step, no device state.
+  static std::unique_ptr<AdamState> snapshot(std::vector<double> m, std::vector<double> v,
+                                             int64_t step) {
+    auto s = std::make_unique<AdamState>(0);
+    s->n_ = m.size() / kScalars;
+    s->pm_ = std::move(m);
+    s->pv_ = std::move(v);
+    s->step_ = step;
+    s->pending_ = true;
+    return s;
+  }
+
  private:
+  void moments(std::vector<double>& m, std::vector<double>& v) const {
+    if (pending_ || !h_) {
+      m = pm_;
+      v = pv_;
+      m.resize(n_ * kScalars, 0.0);
+      v.resize(n_ * kScalars, 0.0);
+      return;
+    }
+    m.assign(n_ * kScalars, 0.0);
+    v.assign(n_ * kScalars, 0.0);
+    int64_t st = 0;
+    check(dsg_model_adam_state(Context::current().get(), h_, m.data(), v.data(), &st));
+  }
   dsg_model h_ = nullptr;
   size_t n_ = 0;
+  int64_t dev_n_ = -1;
   int64_t step_ = 0;
+  std::vector<double> pm_, pv_;
+  bool pending_ = false;
 };
 
+// CheckpointSink (trainer.hpp:119-120) with the drop-in's AdamState, whose
+// serialize() gives the reference's payload (runtime.hpp:262-275 writes it
+// to the .adam sidecar). Reference callers that name the type in the lambda
+// parameter switch `const AdamState&` to `const auto&`.
+using CheckpointSink =
+    std::function<void(const SplatModel&, const AdamState&, int64_t iteration, double loss)>;
+
 // train_partition_full (trainer.hpp:140-211): the whole loop on the device.
-// CheckpointSink is not supported on the device path (the reference's
-// AdamState cannot be populated from outside); pass nullptr.
 inline TrainResult train_partition_full(const SplatModel& input,
                                         const std::vector<TrainView>& views,
                                         const TrainConfig& cfg, int shards = 1,
@@ -309,8 +394,6 @@ inline TrainResult train_partition_full(const SplatModel& input,
   if (views.empty()) throw Error(ErrorCode::NoViews, "training requires at least one view");
   if (shards < 1) throw Error(ErrorCode::InvalidArgument, "shards must be >= 1");
   for (const auto& v : views) v.validate();
-  if (checkpoint)
-    throw Error(ErrorCode::InvalidArgument, "checkpoint sinks are not supported on the device path");
   Context& ctx = Context::current();
   TrainResult result;
   result.model = input;
@@ -335,10 +418,29 @@ inline TrainResult train_partition_full(const SplatModel& input,
   dsg_train_config tc = detail::train_of(cfg);
   struct Ctx {
     const ProgressSink* p;
-  } pc{&progress};
+    const CheckpointSink* c;
+    const SplatModel* input;
+    dsg_ctx ctx;
+  } pc{&progress, &checkpoint, &input, ctx.get()};
   auto cb = [](int64_t it, double loss, void* u) { (*static_cast<Ctx*>(u)->p)(it, loss); };
-  check(dsg_train(ctx.get(), dm.h, dv, &tc, shards, progress ? +cb : nullptr, &pc,
-                  &result.final_loss, nullptr));
+  // checkpoint: the model and its moments as the reference hands them over
+  auto ck = [](int64_t iter, double loss, dsg_model model, void* u) {
+    Ctx& c = *static_cast<Ctx*>(u);
+    int64_t n = 0, it = 0, steps = 0;
+    check(dsg_model_info(model, &n, &it, &steps));
+    std::vector<double> p(14 * static_cast<size_t>(n)), m(p.size()), v(p.size());
+    int32_t op = -1;
+    check(dsg_model_download(c.ctx, model, p.data(), n, &n, &it, &op));
+    check(dsg_model_adam_state(c.ctx, model, m.data(), v.data(), &steps));
+    SplatModel snap;
+    snap.origin_partition = c.input->origin_partition;
+    detail::params_to(p, snap);
+    snap.iteration = it;
+    auto adam = AdamState::snapshot(std::move(m), std::move(v), steps);
+    (*c.c)(snap, *adam, iter, loss);
+  };
+  check(dsg_train_checkpointed(ctx.get(), dm.h, dv, &tc, shards, progress ? +cb : nullptr, &pc,
+                               checkpoint ? +ck : nullptr, &pc, &result.final_loss, nullptr));
   // densify/prune may have resized the model on the device
   int64_t n = 0, it = 0, adam_steps = 0;
   check(dsg_model_info(dm.h, &n, &it, &adam_steps));

@@ -57,6 +57,7 @@ class dsg_train_config(C.Structure):
 
 
 PROGRESS_FN = C.CFUNCTYPE(None, C.c_int64, C.c_double, C.c_void_p)
+CHECKPOINT_FN = C.CFUNCTYPE(None, C.c_int64, C.c_double, C.c_void_p, C.c_void_p)
 
 _lib = None
 _lock = threading.Lock()
@@ -380,14 +381,45 @@ class AdamState:
         return self.model.info()[2]
 
 
+class AdamSnapshot:
+    """The optimizer state a CheckpointSink receives (trainer.hpp:119-120):
+    moments and step of the device AdamState; serialize() is the reference's
+    payload [step, size, m..., v...] (adam.hpp:103-112)."""
+
+    def __init__(self, m, v, step: int):
+        self.m, self.v, self.step = m, v, int(step)
+
+    def size(self) -> int:
+        return self.m.shape[0]
+
+    def step_count(self) -> int:
+        return self.step
+
+    def serialize(self) -> np.ndarray:
+        return np.concatenate([[float(self.step), float(self.size())], self.m.ravel(),
+                               self.v.ravel()])
+
+
 def train_device(dmodel: DeviceModel, dviews: DeviceViews, cfg: TrainConfig, shards: int = 1,
-                 progress=None, loss_trace: bool = False):
-    """The device-resident training loop (dsg_train); returns (final_loss, trace)."""
+                 progress=None, loss_trace: bool = False, checkpoint=None, origin=None):
+    """The device-resident training loop (dsg_train); returns (final_loss, trace).
+
+    checkpoint(model: SplatModel, adam: AdamSnapshot, iteration, loss) is the
+    reference's CheckpointSink (every checkpoint_interval steps and at the end)."""
     fl = C.c_double()
     trace = np.zeros(max(cfg.iterations, 1)) if loss_trace else None
     cb = PROGRESS_FN(lambda it, loss, user: progress(it, loss)) if progress else None
-    _check(lib().dsg_train(dmodel.ctx.h, dmodel.h, dviews.h, C.byref(train_struct(cfg)),
-                           C.c_int32(shards), cb, None, C.byref(fl), _p(trace)))
+
+    def _ck(it, loss, model_h, user):
+        snap = dmodel.download()
+        snap.origin_partition = origin
+        m, v, st = dmodel.adam_state()
+        checkpoint(snap, AdamSnapshot(m, v, st), it, loss)
+
+    ck = CHECKPOINT_FN(_ck) if checkpoint else None
+    _check(lib().dsg_train_checkpointed(dmodel.ctx.h, dmodel.h, dviews.h,
+                                        C.byref(train_struct(cfg)), C.c_int32(shards), cb, None,
+                                        ck, None, C.byref(fl), _p(trace)))
     return fl.value, (trace[: cfg.iterations] if trace is not None else None)
 
 
@@ -401,14 +433,22 @@ def train_partition_full(model: SplatModel, views, cfg: TrainConfig, shards: int
         raise DsplatError(ErrorCode.NoViews, "training requires at least one view")
     if shards < 1:
         raise DsplatError(ErrorCode.InvalidArgument, "shards must be >= 1")
+    import time
+    t0 = time.perf_counter()
     dm = ctx.scratch_model(model)
+    t1 = time.perf_counter()
     dv = HostRefViews(ctx, views)  # scheduled views streamed from host memory
-    fl, trace = train_device(dm, dv, cfg, shards, progress, loss_trace)
+    t2 = time.perf_counter()
+    fl, trace = train_device(dm, dv, cfg, shards, progress, loss_trace, checkpoint=checkpoint,
+                             origin=model.origin_partition)
+    t3 = time.perf_counter()
     out = dm.download()
     out.origin_partition = model.origin_partition
     res = TrainResult(out, fl, len(model), len(out))
     if trace is not None:
         res.loss_trace = trace
+    ctx.last_phases = {"upload_s": t1 - t0, "views_s": t2 - t1, "train_s": t3 - t2,
+                       "download_s": time.perf_counter() - t3}
     return res
 
 

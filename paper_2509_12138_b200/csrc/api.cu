@@ -80,6 +80,7 @@ struct dsg_ctx_s {
   StageTimer timer;
   bool timer_init = false;
   ModelDev spare;  // densification output storage (swapped with the model's)
+  DensifyScratch dscratch;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   // end-to-end mode: next step's view is copied on its own stream into the
   // other of two device slots while this step computes
@@ -340,7 +341,7 @@ void reset_optimizer(dsg_ctx ctx, ModelDev& m) {
   cudaStream_t st = ctx->stream;
   DSG_CUDA_CHECK(cudaMemsetAsync(m.m.get(), 0, sizeof(float) * kParams * m.cap, st));
   DSG_CUDA_CHECK(cudaMemsetAsync(m.v.get(), 0, sizeof(float) * kParams * m.cap, st));
-  DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_norm.get(), 0, sizeof(float) * m.cap, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_norm.get(), 0, sizeof(double) * m.cap, st));
   DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_count.get(), 0, sizeof(int32_t) * m.cap, st));
   m.adam_step = 0;
 }
@@ -490,6 +491,10 @@ class HostPool {
       workers_.emplace_back([this] { loop(); });
   }
   ~HostPool() {
+    if (getpid() != pid_) {  // forked child: the workers (and mu_'s owner) are the parent's
+      for (auto& t : workers_) t.detach();
+      return;
+    }
     {
       std::lock_guard<std::mutex> lk(mu_);
       stop_ = true;
@@ -758,6 +763,34 @@ int dsg_model_adam_state(dsg_ctx ctx, dsg_model model, double* mo, double* vo, i
                                      cudaMemcpyDeviceToHost, ctx->stream));
       DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     }
+  });
+}
+
+int dsg_model_adam_restore(dsg_ctx ctx, dsg_model model, const double* mo, const double* vo,
+                           int64_t n, int64_t step) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    if (n != m.n) fail(kMismatchedCounts, "moment count differs from the device model");
+    if (step < 0) fail(kInvalidArgument, "negative Adam step");
+    cudaStream_t st = ctx->stream;
+    if (n > 0) {
+      double* d = ctx->stage_d.ensure(kParams * n);
+      for (int k = 0; k < 2; ++k) {
+        const double* src = k == 0 ? mo : vo;
+        float* dst = k == 0 ? m.m.get() : m.v.get();
+        if (src) {
+          DSG_CUDA_CHECK(cudaMemcpyAsync(d, src, sizeof(double) * kParams * n,
+                                         cudaMemcpyHostToDevice, st));
+          k_aos_to_planar<<<nblk(n), 256, 0, st>>>(d, n, kParams, dst, m.cap);
+          count_launch();
+        } else {
+          DSG_CUDA_CHECK(cudaMemsetAsync(dst, 0, sizeof(float) * kParams * m.cap, st));
+        }
+      }
+    }
+    m.adam_step = step;
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
   });
 }
 
@@ -1084,6 +1117,14 @@ extern "C" {
 int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_config* cfg,
               int32_t shards, dsg_progress_fn progress, void* user, double* final_loss,
               double* loss_trace) {
+  return dsg_train_checkpointed(ctx, model, views, cfg, shards, progress, user, nullptr, nullptr,
+                                final_loss, loss_trace);
+}
+
+int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
+                           const dsg_train_config* cfg, int32_t shards, dsg_progress_fn progress,
+                           void* user, dsg_checkpoint_fn checkpoint, void* ckpt_user,
+                           double* final_loss, double* loss_trace) {
   return guarded([&] {
     validate_train(cfg);
     if (!views || views->n <= 0) fail(kNoViews, "training requires at least one view");
@@ -1229,7 +1270,7 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
       m.iteration += 1;
       // densify at (it+1) % interval == 0 while (it+1) < stop (trainer.hpp:195-202)
       if (cfg->densify_interval > 0 && (it + 1) % cfg->densify_interval == 0 && (it + 1) < until)
-        densify_dev(m, ctx->spare, cfg->prune_opacity, cfg->densify_grad_threshold,
+        densify_dev(m, ctx->spare, ctx->dscratch, cfg->prune_opacity, cfg->densify_grad_threshold,
                     cfg->split_scale_threshold, drng, ctx->frame.scan, st);
       tm.mark(9, st);
       if (tm.on) {
@@ -1240,11 +1281,16 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
           stage[s] += ms;
         }
       }
-      if (progress) {
+      // CheckpointSink at the interval, then ProgressSink (trainer.hpp:204-207);
+      // the callback may read the model and its Adam moments through the ABI
+      const bool ckpt_now = checkpoint && cfg->checkpoint_interval > 0 &&
+                            (it + 1) % cfg->checkpoint_interval == 0;
+      if (progress || ckpt_now) {
         double l;
         DSG_CUDA_CHECK(cudaMemcpyAsync(&l, trace + it, sizeof(double), cudaMemcpyDeviceToHost, st));
         DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-        progress(it + 1, l, user);
+        if (ckpt_now) checkpoint(m.iteration, l, model, ckpt_user);
+        if (progress) progress(it + 1, l, user);
       }
     }
     DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_end, st));
@@ -1258,6 +1304,7 @@ int dsg_train(dsg_ctx ctx, dsg_model model, dsg_views views, const dsg_train_con
     DSG_CUDA_CHECK(cudaMemcpy(tr.data(), trace, sizeof(double) * iters, cudaMemcpyDeviceToHost));
     if (final_loss) *final_loss = tr.back();
     if (loss_trace) std::memcpy(loss_trace, tr.data(), sizeof(double) * iters);
+    if (checkpoint) checkpoint(m.iteration, tr.back(), model, ckpt_user);  // trainer.hpp:209
   });
 }
 

@@ -89,8 +89,8 @@ __global__ void __launch_bounds__(256, DSG_ADAM_MINB) k_adam(AdamArgs a) {
 #pragma unroll
   for (int k = 0; k < kParams; ++k) a.params[k * P + i] = p[k];
   if (a.accumulate_stats && a.touch[i] > 0) {
-    float dx = a.dmean[i], dy = a.dmean[P + i];
-    a.stat_norm[i] += sqrtf(dx * dx + dy * dy);
+    const double dx = a.dmean[i], dy = a.dmean[P + i];
+    a.stat_norm[i] += sqrt(dx * dx + dy * dy);  // d_mean2d.norm() (trainer.hpp:189-193)
     a.stat_count[i] += 1;
   }
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ double normal_at(uint64_t state, uint64_t k) {  // rn
 
 // 0 prune, 1 keep, 2 clone, 3 split (trainer.hpp:68-101)
 __global__ void k_densify_classify(const float* __restrict__ P, int64_t pitch, int64_t n,
-                                   const float* __restrict__ sg, const int32_t* __restrict__ tc,
+                                   const double* __restrict__ sg, const int32_t* __restrict__ tc,
                                    double prune_opacity, double grad_thr, double split_thr,
                                    uint8_t* __restrict__ cls, uint32_t* __restrict__ c_main,
                                    uint32_t* __restrict__ c_app, uint32_t* __restrict__ c_split) {
@@ -53,7 +53,7 @@ __global__ void k_densify_classify(const float* __restrict__ P, int64_t pitch, i
   const double op = 1.0 / (1.0 + exp(-(double)P[10 * pitch + i]));
   uint8_t c = 0;
   if (!(op < prune_opacity)) {
-    const double mg = tc[i] > 0 ? (double)sg[i] / tc[i] : 0.0;
+    const double mg = tc[i] > 0 ? sg[i] / tc[i] : 0.0;
     if (mg > grad_thr) {
       const double s = fmax(exp((double)P[3 * pitch + i]),
                             fmax(exp((double)P[4 * pitch + i]), exp((double)P[5 * pitch + i])));
@@ -132,7 +132,7 @@ __global__ void k_densify_scatter(const float* __restrict__ P, const float* __re
   }
 }
 
-__global__ void k_mu_bounds(const float* __restrict__ P, int64_t pitch, int64_t n, float* out) {
+__global__ void k_mu_bounds(const float* __restrict__ P, int64_t pitch, int64_t n, int* out) {
   // out[0..2] = min, out[3..5] = max (float atomics via ordered ints)
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -141,8 +141,8 @@ __global__ void k_mu_bounds(const float* __restrict__ P, int64_t pitch, int64_t 
     const float v = P[c * pitch + i];
     const int iv = __float_as_int(v);
     const int key = iv >= 0 ? iv : iv ^ 0x7fffffff;  // monotone int key
-    atomicMin(reinterpret_cast<int*>(out) + c, key);
-    atomicMax(reinterpret_cast<int*>(out) + 3 + c, key);
+    atomicMin(out + c, key);
+    atomicMax(out + 3 + c, key);
   }
 }
 
@@ -150,7 +150,8 @@ inline unsigned nb(int64_t n) { return (unsigned)std::max<int64_t>(1, (n + 255) 
 
 }  // namespace
 
-DensifyResult densify_dev(ModelDev& m, ModelDev& spare, double prune_opacity, double grad_thr,
+DensifyResult densify_dev(ModelDev& m, ModelDev& spare, DensifyScratch& ds, double prune_opacity,
+                          double grad_thr,
                           double split_thr_cfg, uint64_t& rng_state, ScanScratch& sc,
                           cudaStream_t st) {
   DensifyResult r;
@@ -161,7 +162,7 @@ DensifyResult densify_dev(ModelDev& m, ModelDev& spare, double prune_opacity, do
   if (split_thr <= 0.0) {
     double diag = 0.0;
     if (n > 0) {
-      DevBuf<float> b;
+      DevBuf<int>& b = ds.box;
       b.ensure(6);
       int init[6] = {0x7fffffff, 0x7fffffff, 0x7fffffff, (int)0x80000000, (int)0x80000000,
                      (int)0x80000000};
@@ -187,8 +188,8 @@ DensifyResult densify_dev(ModelDev& m, ModelDev& spare, double prune_opacity, do
     }
     split_thr = 0.02 * diag;
   }
-  DevBuf<uint8_t> cls;
-  DevBuf<uint32_t> cm, ca, cs;
+  DevBuf<uint8_t>& cls = ds.cls;
+  DevBuf<uint32_t>&cm = ds.cm, &ca = ds.ca, &cs = ds.cs;
   cls.ensure(std::max<int64_t>(n, 1));
   cm.ensure(n + 1);
   ca.ensure(n + 1);
@@ -225,7 +226,7 @@ DensifyResult densify_dev(ModelDev& m, ModelDev& spare, double prune_opacity, do
   m.stat_norm.ensure(m.cap);
   m.stat_count.ensure(m.cap);
   m.n = n_new;
-  DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_norm.get(), 0, sizeof(float) * m.cap, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_norm.get(), 0, sizeof(double) * m.cap, st));
   DSG_CUDA_CHECK(cudaMemsetAsync(m.stat_count.get(), 0, sizeof(int32_t) * m.cap, st));
   r.after = n_new;
   r.splits = tot[2];

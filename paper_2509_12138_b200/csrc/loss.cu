@@ -25,7 +25,6 @@ namespace {
 constexpr int kW = 11, kR = 5;
 constexpr int kB = 16;             // output block edge
 constexpr int kE = kB + 2 * kR;    // 26: block plus apron
-__constant__ double c_win[kW];     // 1-D factor of the window, sum of outer product = 1
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;  // ssim.hpp:12-13
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -60,6 +59,9 @@ struct LossArgs {
   float* dL;           // planar [3][npix]
   double* loss_out;
   int nblocks;
+  // 1-D factor of the SSIM window (outer product sums to 1, ssim.hpp:17-31);
+  // a kernel parameter, so every device and context sees it with the launch
+  double win[kW];
 };
 
 __global__ void __launch_bounds__(kB* kB) k_ssim_stats(LossArgs a) {
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kB* kB) k_ssim_stats(LossArgs a) {
       double s0 = 0, s1 = 0, s2 = 0, s3 = 0, s4 = 0;
 #pragma unroll
       for (int k = 0; k < kW; ++k) {
-        double wk = c_win[k], xv = xs[r][c + k], yv = ys[r][c + k];
+        double wk = a.win[k], xv = xs[r][c + k], yv = ys[r][c + k];
         s0 += wk * xv;
         s1 += wk * yv;
         s2 += wk * (xv * xv);
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kB* kB) k_ssim_stats(LossArgs a) {
       double mx = 0, my = 0, sxx = 0, syy = 0, sxy = 0;
 #pragma unroll
       for (int k = 0; k < kW; ++k) {
-        double wk = c_win[k];
+        double wk = a.win[k];
         mx += wk * hs[0][ty + k][tx];
         my += wk * hs[1][ty + k][tx];
         sxx += wk * hs[2][ty + k][tx];
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kB* kB) k_loss_grad(LossArgs a) {
         double s0 = 0, s1 = 0, s2 = 0;
 #pragma unroll
         for (int k = 0; k < kW; ++k) {
-          double wk = c_win[k];
+          double wk = a.win[k];
           s0 += wk * ps[0][r][c + k];
           s1 += wk * ps[1][r][c + k];
           s2 += wk * ps[2][r][c + k];
@@ -207,7 +209,7 @@ __global__ void __launch_bounds__(kB* kB) k_loss_grad(LossArgs a) {
       __syncthreads();
 #pragma unroll
       for (int k = 0; k < kW; ++k) {
-        double wk = c_win[k];
+        double wk = a.win[k];
         corr[0] += wk * hs[0][ty + k][tx];
         corr[1] += wk * hs[1][ty + k][tx];
         corr[2] += wk * hs[2][ty + k][tx];
@@ -252,25 +254,21 @@ __global__ void __launch_bounds__(256) k_loss_final(LossArgs a) {
   }
 }
 
-void ensure_window() {
-  static bool done = false;
-  if (done) return;
-  double g[kW], sum = 0.0;
+// gaussian_window (ssim.hpp:17-31) factored: g_k / sum(g), sigma 1.5
+void fill_window(double* g) {
+  double sum = 0.0;
   for (int k = 0; k < kW; ++k) {
     int d = k - kR;
     g[k] = exp(-(double)(d * d) / (2.0 * 1.5 * 1.5));
     sum += g[k];
   }
   for (int k = 0; k < kW; ++k) g[k] /= sum;
-  DSG_CUDA_CHECK(cudaMemcpyToSymbol(c_win, g, sizeof g));
-  done = true;
 }
 
 }  // namespace
 
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
                      double lambda, cudaStream_t st, double* out) {
-  ensure_window();
   const int64_t npix = (int64_t)width * height;
   dim3 grid((width + kB - 1) / kB, (height + kB - 1) / kB);
   const int nblocks = grid.x * grid.y;
@@ -294,6 +292,7 @@ void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, 
   a.dL = f.dL.get();
   a.loss_out = out ? out : f.loss_out.get();
   a.nblocks = nblocks;
+  fill_window(a.win);
   k_ssim_stats<<<grid, kB * kB, 0, st>>>(a);
   count_launch();
   k_loss_grad<<<grid, kB * kB, 0, st>>>(a);

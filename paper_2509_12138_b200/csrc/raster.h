@@ -17,7 +17,7 @@ constexpr int kSegMin = DSG_SEG_MIN;
 #define DSG_SEG_DIV 8192
 #endif
 constexpr int kSegDiv = DSG_SEG_DIV;
-constexpr int kUnitPlanes = 14;  // per-unit per-pixel planes (blend.cu UnitPlane)
+constexpr int kUnitPlanes = 15;  // per-unit per-pixel planes (blend.cu UnitPlane)
 #ifndef DSG_SPLIT_MIN
 #define DSG_SPLIT_MIN 32768
 #endif
@@ -78,7 +78,7 @@ struct Frame {
   DevBuf<uint32_t> counters;
   DevBuf<uint32_t> amb, tile_unit;  // termination fix-up: flagged pixels, tile -> first unit
   // per pixel (planar fp32)
-  DevBuf<float> rgb, T, dL;
+  DevBuf<float> rgb, T, dL, Tband;
   DevBuf<uint32_t> last;
   DevBuf<int32_t> ncontrib;
   // backward partials: [n_dup][8 sub-tiles][8] (values 0..7) then [n_dup][8] (value 8)
@@ -127,7 +127,8 @@ struct ModelDev {
   int64_t iteration = 0;
   int32_t origin_partition = -1;
   int64_t adam_step = 0;
-  DevBuf<float> params, grads, m, v, dmean, stat_norm;
+  DevBuf<float> params, grads, m, v, dmean;
+  DevBuf<double> stat_norm;  // screen_grad_norm (gradient.hpp:16), fp64 like the reference
   DevBuf<int32_t> touch, stat_count;
   void reserve(int64_t c);
 };
@@ -153,7 +154,7 @@ struct AdamArgs {
   float* v;
   const float* dmean;
   const int32_t* touch;
-  float* stat_norm;
+  double* stat_norm;
   int32_t* stat_count;
   int64_t pitch, n;
   float lr[5];
@@ -218,7 +219,14 @@ int64_t merge_compact_dev(const float* src, int64_t spitch, int64_t n, int axis,
 struct DensifyResult {
   int64_t before = 0, after = 0, splits = 0;
 };
-DensifyResult densify_dev(ModelDev& m, ModelDev& spare, double prune_opacity, double grad_thr,
+// Per-context scratch of densify_dev (classes and three flag scans).
+struct DensifyScratch {
+  DevBuf<uint8_t> cls;
+  DevBuf<uint32_t> cm, ca, cs;
+  DevBuf<int> box;
+};
+DensifyResult densify_dev(ModelDev& m, ModelDev& spare, DensifyScratch& ds, double prune_opacity,
+                          double grad_thr,
                           double split_thr_cfg, uint64_t& rng_state, ScanScratch& sc,
                           cudaStream_t st);
 

@@ -4,6 +4,7 @@
 // Built here by tests/cpp/Makefile (needs the reference headers); the binary
 // travels to the GPU box and is run by tests/test_cpp_dropin.py.
 #include <cmath>
+#include <optional>
 #include <cstdio>
 #include <string>
 
@@ -121,6 +122,104 @@ int main() {
     EXPECT(std::abs(ra.final_loss - rb.final_loss) <= 2e-3 * ra.final_loss, "train loss %g vs %g",
            ra.final_loss, rb.final_loss);
     EXPECT(rb.model.iteration == init.iteration + 20, "iteration %ld", (long)rb.model.iteration);
+  }
+  // CheckpointSink (trainer.hpp:204-209): same calls, iterations, losses and
+  // serialize() payload shape; moments track the reference's
+  {
+    Camera c = cam(40);
+    SplatModel init = scene(31, 10, 1.0);
+    init.origin_partition = 2;
+    TrainView v;
+    v.cam = c;
+    v.ground_truth = render(scene(32, 10, 1.0), c, cfg).color;
+    v.mask = Image(40, 40, 1, 1.0);
+    TrainConfig tc;
+    tc.iterations = 12;
+    tc.seed = 5;
+    tc.checkpoint_interval = 5;
+    struct Ck {
+      int64_t iter;
+      double loss;
+      std::vector<double> adam;
+      size_t n;
+      std::optional<int> origin;
+    };
+    std::vector<Ck> ca, cb;
+    train_partition_full(init, {v}, tc, 1,
+                         [&](const SplatModel& m, const AdamState& a, int64_t it, double l) {
+                           ca.push_back({it, l, a.serialize(), m.size(), m.origin_partition});
+                         });
+    b200::train_partition_full(init, {v}, tc, 1,
+                               [&](const SplatModel& m, const auto& a, int64_t it, double l) {
+                                 cb.push_back({it, l, a.serialize(), m.size(), m.origin_partition});
+                               });
+    EXPECT(ca.size() == 3 && cb.size() == ca.size(), "checkpoint calls %zu vs %zu", ca.size(),
+           cb.size());
+    for (size_t k = 0; k < ca.size() && k < cb.size(); ++k) {
+      EXPECT(ca[k].iter == cb[k].iter, "checkpoint %zu iteration %ld vs %ld", k, (long)ca[k].iter,
+             (long)cb[k].iter);
+      EXPECT(std::abs(ca[k].loss - cb[k].loss) <= 2e-3 * ca[k].loss, "checkpoint %zu loss", k);
+      EXPECT(ca[k].adam.size() == cb[k].adam.size() && ca[k].adam[0] == cb[k].adam[0] &&
+                 ca[k].adam[1] == cb[k].adam[1], "checkpoint %zu adam header", k);
+      EXPECT(ca[k].n == cb[k].n && ca[k].origin == cb[k].origin, "checkpoint %zu model", k);
+      double vmax = 0, verr = 0;
+      const size_t half = (ca[k].adam.size() - 2) / 2;
+      for (size_t i = 2 + half; i < ca[k].adam.size() && i < cb[k].adam.size(); ++i) {
+        vmax = std::max(vmax, std::abs(ca[k].adam[i]));
+        verr = std::max(verr, std::abs(ca[k].adam[i] - cb[k].adam[i]));
+      }
+      EXPECT(verr <= 0.05 * vmax, "checkpoint %zu second moments %g of %g", k, verr, vmax);
+    }
+  }
+  // AdamState resize / remap / serialize / step (adam.hpp:24-112)
+  {
+    Camera c = cam(32);
+    SplatModel m = scene(61, 6, 1.0);
+    RenderOutput o = render(m, c, cfg);
+    TrainView v;
+    v.cam = c;
+    v.ground_truth = render(scene(62, 6, 1.0), c, cfg).color;
+    v.mask = Image(32, 32, 1, 1.0);
+    GradientBuffer g = backward(m, c, cfg, o, masked_loss(o.color, v, 0.2).dL_dpixels);
+    AdamState ra(m.size());
+    b200::AdamState rb(m.size());
+    SplatModel ma = m, mb = m;
+    AdamState::GroupRates lr{1e-3, 5e-3, 1e-3, 5e-2, 5e-3};
+    ra.step(ma, g, lr);
+    rb.step(mb, g, lr);
+    std::vector<int32_t> src{3, -1, 0, 0, 5, -1, 2};
+    ra.remap(src);
+    rb.remap(src);
+    auto sa = ra.serialize(), sb = rb.serialize();
+    EXPECT(sa.size() == sb.size() && sa[0] == sb[0] && sa[1] == sb[1], "remap payload header");
+    double err = 0, mx = 0;
+    for (size_t i = 2; i < sa.size() && i < sb.size(); ++i) {
+      err = std::max(err, std::abs(sa[i] - sb[i]) / std::max(std::abs(sa[i]), 1e-30));
+      mx = std::max(mx, std::abs(sa[i]));
+    }
+    EXPECT(err <= 1e-5, "remapped moments rel err %g", err);
+    // untouched scalars keep their exact value after a step (zero update)
+    SplatModel m7 = m;
+    m7.gaussians.push_back(m.gaussians[0]);
+    GradientBuffer g7 = g;
+    g7.d_mu.push_back({0, 0, 0});
+    g7.d_log_scale.push_back({0, 0, 0});
+    g7.d_rot.push_back({0, 0, 0, 0});
+    g7.d_opacity_logit.push_back(0.0);
+    g7.d_color.push_back({0, 0, 0});
+    g7.d_mean2d.push_back({0, 0});
+    g7.touch_count.push_back(0);
+    g7.d_mu[1] = {0, 0, 0};  // entry 1: fresh moments (remap -1) and no gradient
+    SplatModel pa = m7, pb = m7;
+    pb.gaussians[1].mu.x = 0.1234567890123;  // not fp32-exact; zero update keeps it exact
+    pa.gaussians[1].mu.x = pb.gaussians[1].mu.x;
+    ra.step(pa, g7, lr);
+    rb.step(pb, g7, lr);
+    EXPECT(pb.gaussians[1].mu.x == 0.1234567890123 && pa.gaussians[1].mu.x == pb.gaussians[1].mu.x,
+           "zero-update scalar changed: %.17g", pb.gaussians[1].mu.x);
+    EXPECT(ra.step_count() == rb.step_count() && rb.step_count() == 2, "step count");
+    rb.resize(3);
+    EXPECT(rb.size() == 3 && rb.serialize().size() == 2 + 2 * 3 * 14, "resize");
   }
   // densification resizes the model on the device; the drop-in returns it whole
   {

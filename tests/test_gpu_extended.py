@@ -271,3 +271,28 @@ def test_model_transfer_round_trip(ctx, n):
     dm.upload(SplatModel(P[: max(1, n // 2)]))
     np.testing.assert_array_equal(dm.download().params,
                                   P[: max(1, n // 2)].astype(np.float32).astype(np.float64))
+
+
+def test_checkpoint_sink(orc, ctx):
+    """CheckpointSink (trainer.hpp:119-120, 204-209): called every
+    checkpoint_interval steps and once at the end with the model, its Adam
+    state (serialize() = [step, size, m..., v...], adam.hpp:103-112), the
+    model iteration and the step's loss."""
+    cam = make_camera(40)
+    target = fp32_exact(random_scene(24, 10))
+    model = fp32_exact(random_scene(25, 10))
+    model.origin_partition = 3
+    view = TrainView(cam, orc.render(target, cam, RenderConfig()).color, np.ones((40, 40)))
+    calls = []
+    cfg = TrainConfig(iterations=12, seed=5, checkpoint_interval=5)
+    res = api.train_partition_full(
+        model, [view], cfg, ctx=ctx, loss_trace=True,
+        checkpoint=lambda m, a, it, loss: calls.append((m, a.serialize(), it, loss)))
+    assert [c[2] for c in calls] == [5, 10, 12]
+    for m, payload, it, loss in calls:
+        assert m.iteration == it and m.origin_partition == 3
+        assert payload[0] == it and payload[1] == len(m) and len(payload) == 2 + 28 * len(m)
+        assert loss == res.loss_trace[min(it, 12) - 1]
+    np.testing.assert_array_equal(calls[-1][0].params, res.model.params)
+    ref = orc.train_partition_full(model, [view], TrainConfig(iterations=12, seed=5))
+    assert abs(ref.final_loss - res.final_loss) <= 1e-4 * ref.final_loss
