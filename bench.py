@@ -429,6 +429,7 @@ def run_ours(args, dist: Dist):
     stage_ms = {s: float(v) / pk for s, v in zip(api.STAGES, stages)}
     fs = api.frame_stats(ctx)
     n_dup, nv_vis = fs["n_dup"], fs["n_visible"]
+    work = api.frame_work(ctx)  # composited pairs C and fp64 termination fix-ups, last view
 
     # render Mpix/s on the test views (forward only, device-timed)
     test_cams = [inp["rig"][i] for i in inp["test_idx"]]
@@ -502,6 +503,7 @@ def run_ours(args, dist: Dist):
         "wall_s": round(wall_max, 4),
         "stage_ms": {k: round(v, 4) for k, v in stage_ms.items()},
         "n_dup": n_dup,
+        "frame_work": work,
         "e2e": {"value": round(total_iters / e_max, 3), "unit": "it/s",
                 "api": "api.train_partition_full(SplatModel, [TrainView], TrainConfig) "
                        "(trainer.hpp:140): host doubles in, reference-layout views, host doubles out",

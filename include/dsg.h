@@ -110,6 +110,28 @@ int dsg_model_adam_state(dsg_ctx ctx, dsg_model model, double* m, double* v, int
 int dsg_model_adam_restore(dsg_ctx ctx, dsg_model model, const double* m, const double* v,
                            int64_t n, int64_t step);
 
+/* ---- float64 PLY (ply_io.hpp:89-221) --------------------------------------- */
+/* write_splat_ply / read_splat_ply of a device model: byte-identical to
+ * serialize_splat_ply of the model's values; load resets the optimizer and
+ * takes iteration / origin_partition from the header comments. */
+int dsg_model_save_ply(dsg_ctx ctx, dsg_model model, const char* path);
+int dsg_model_load_ply(dsg_ctx ctx, dsg_model model, const char* path);
+/* write_cloud_ply / read_cloud_ply: positions, normals, colors [n][3]
+ * (normals/colors may be NULL: zeros on write, skipped on read); load with
+ * positions NULL is a size query into *n. */
+int dsg_cloud_save_ply(const char* path, const double* positions, const double* normals,
+                       const double* colors, int64_t n);
+int dsg_cloud_load_ply(const char* path, double* positions, double* normals, double* colors,
+                       int64_t capacity, int64_t* n);
+
+/* ---- evaluation (metrics.hpp:20-38, runtime.hpp:483-492) ---------------------- */
+/* psnr (capped at 99) and mean windowed SSIM of two HWC double RGB images. */
+int dsg_image_metrics(dsg_ctx ctx, const double* a, const double* b, int32_t width,
+                      int32_t height, double* psnr, double* ssim);
+/* psnr / ssim of render(model) against render(truth) at cam, on the device. */
+int dsg_eval_view(dsg_ctx ctx, dsg_model model, dsg_model truth, const dsg_camera* cam,
+                  const dsg_render_config* cfg, double* psnr, double* ssim);
+
 /* ---- render path ---------------------------------------------------------- */
 /* render (render.hpp:160-205). Outputs (each may be NULL): rgb [h][w][3],
  * alpha [h][w], n_contrib [h][w], splat_order (capacity n) and its length,
@@ -251,6 +273,10 @@ int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const ds
 int64_t dsg_launch_count(void);
 /* Visible splats and tile duplicates of the last view binned on ctx. */
 int dsg_frame_stats(dsg_ctx ctx, int64_t* n_visible, int64_t* n_dup);
+/* Work of the last forward on ctx: composited (pixel, splat) pairs (the sum
+ * of n_contrib, the blend kernels' work count C) and the pixels
+ * whose termination was re-decided in fp64. */
+int dsg_frame_work(dsg_ctx ctx, int64_t* composited, int64_t* term_fixups);
 /* Forward-render n cameras `repeats` times back to back on the device;
  * *ms = CUDA-event time (render Mpix/s measurement). */
 int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32_t n,

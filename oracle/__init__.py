@@ -261,6 +261,28 @@ class _CpuImpl:
             res.loss_trace = trace
         return res
 
+    # -- float64 PLY (ply_io.hpp:89-221; oracle/_ref only) ---------------------
+    def write_splat_ply(self, path: str, model: SplatModel):
+        P = self._params(model)
+        op = -1 if model.origin_partition is None else int(model.origin_partition)
+        self._check(self.lib.orc_write_splat_ply(path.encode(), _p(P), C.c_int64(P.shape[0]),
+                                                 C.c_int64(model.iteration), C.c_int32(op)))
+
+    def read_splat_ply(self, path: str) -> SplatModel:
+        n, it, op = C.c_int64(), C.c_int64(), C.c_int32()
+        self._check(self.lib.orc_read_splat_ply(path.encode(), None, C.c_int64(0), C.byref(n),
+                                                C.byref(it), C.byref(op)))
+        P = np.zeros((max(n.value, 1), PARAMS))
+        self._check(self.lib.orc_read_splat_ply(path.encode(), _p(P), C.c_int64(P.shape[0]),
+                                                C.byref(n), C.byref(it), C.byref(op)))
+        return SplatModel(P[: n.value], it.value, None if op.value < 0 else op.value)
+
+    def write_cloud_ply(self, path: str, positions, normals, colors):
+        pos, nrm, col = (np.ascontiguousarray(a, dtype=np.float64).reshape(-1, 3)
+                         for a in (positions, normals, colors))
+        self._check(self.lib.orc_write_cloud_ply(path.encode(), _p(pos), _p(nrm), _p(col),
+                                                 C.c_int64(pos.shape[0])))
+
     def train_partition(self, model, views, cfg, shards: int = 1) -> SplatModel:
         return self.train_partition_full(model, views, cfg, shards).model
 

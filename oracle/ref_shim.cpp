@@ -10,6 +10,7 @@
 #include "dsplat/backward.hpp"
 #include "dsplat/metrics.hpp"
 #include "dsplat/partition.hpp"
+#include "dsplat/ply_io.hpp"
 #include "dsplat/seed.hpp"
 #include "dsplat/trainer.hpp"
 #include "orc_abi.h"
@@ -434,3 +435,40 @@ int orc_rng_uniform(uint64_t seed, int64_t count, double* out) {
 }
 
 }  // extern "C"
+
+// ---- float64 PLY (ply_io.hpp:89-221), reference only -----------------------
+extern "C" int orc_write_splat_ply(const char* path, const double* params, int64_t n,
+                                   int64_t iteration, int32_t origin) {
+  return guarded([&] {
+    SplatModel m = to_model(params, n);
+    m.iteration = iteration;
+    if (origin >= 0) m.origin_partition = origin;
+    write_splat_ply(path, m);
+  });
+}
+
+extern "C" int orc_read_splat_ply(const char* path, double* params, int64_t cap, int64_t* n,
+                                  int64_t* iteration, int32_t* origin) {
+  return guarded([&] {
+    SplatModel m = read_splat_ply(path);
+    *n = static_cast<int64_t>(m.size());
+    *iteration = m.iteration;
+    *origin = m.origin_partition ? *m.origin_partition : -1;
+    if (params && cap >= *n) from_model(m, params);
+  });
+}
+
+extern "C" int orc_write_cloud_ply(const char* path, const double* pos, const double* nrm,
+                                   const double* col, int64_t n) {
+  return guarded([&] {
+    PointCloud pc;
+    pc.points.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+      SurfacePoint& p = pc.points[static_cast<size_t>(i)];
+      p.position = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+      p.normal = {nrm[3 * i], nrm[3 * i + 1], nrm[3 * i + 2]};
+      p.color = {col[3 * i], col[3 * i + 1], col[3 * i + 2]};
+    }
+    write_cloud_ply(path, pc);
+  });
+}

@@ -203,6 +203,14 @@ class DeviceModel:
                                         C.byref(nn), C.byref(it), C.byref(op)))
         return SplatModel(P[: nn.value], it.value, None if op.value < 0 else op.value)
 
+    def save_ply(self, path: str):
+        """write_splat_ply (ply_io.hpp:89-119) straight from the device store."""
+        _check(lib().dsg_model_save_ply(self.ctx.h, self.h, os.fsencode(path)))
+
+    def load_ply(self, path: str):
+        """read_splat_ply (ply_io.hpp:121-158) into this device model."""
+        _check(lib().dsg_model_load_ply(self.ctx.h, self.h, os.fsencode(path)))
+
     def adam_state(self):
         n, _, _ = self.info()
         m = np.zeros((max(n, 1), PARAMS))
@@ -585,6 +593,13 @@ def frame_stats(ctx: Context):
     return {"n_visible": nv.value, "n_dup": nd.value}
 
 
+def frame_work(ctx: Context):
+    """(composited pairs C, termination fix-ups) of the last forward on ctx."""
+    c, f = C.c_int64(), C.c_int64()
+    _check(lib().dsg_frame_work(ctx.h, C.byref(c), C.byref(f)))
+    return {"composited": c.value, "term_fixups": f.value}
+
+
 def render_timed(dmodel: DeviceModel, cams, cfg: RenderConfig, repeats: int = 1) -> float:
     """Device ms to forward-render `cams` `repeats` times (render Mpix/s)."""
     n = len(cams)
@@ -691,3 +706,60 @@ def render_distributed(comm, model: DeviceModel, cam: Camera, cfg: RenderConfig,
                                         C.byref(cam_struct(cam)), C.byref(cfg_struct(cfg)),
                                         _p(rgb), C.byref(ms)))
     return rgb, ms.value
+
+
+# ---- I/O and evaluation (ply_io.hpp, metrics.hpp) --------------------------------
+def write_splat_ply(path: str, model, ctx: Context = None):
+    """write_splat_ply (ply_io.hpp:89-119) of a host or device model."""
+    ctx = ctx or default_context()
+    _as_device_model(model, ctx).save_ply(path)
+
+
+def read_splat_ply(path: str, ctx: Context = None) -> SplatModel:
+    """read_splat_ply (ply_io.hpp:121-158)."""
+    ctx = ctx or default_context()
+    dm = DeviceModel(ctx)
+    dm.load_ply(path)
+    return dm.download()
+
+
+def write_cloud_ply(path: str, positions, normals=None, colors=None):
+    """write_cloud_ply (ply_io.hpp:170-191)."""
+    pos = np.ascontiguousarray(positions, dtype=np.float64).reshape(-1, 3)
+    nrm = None if normals is None else np.ascontiguousarray(normals, dtype=np.float64).reshape(-1, 3)
+    col = None if colors is None else np.ascontiguousarray(colors, dtype=np.float64).reshape(-1, 3)
+    _check(lib().dsg_cloud_save_ply(os.fsencode(path), _p(pos), None if nrm is None else _p(nrm),
+                                    None if col is None else _p(col), C.c_int64(pos.shape[0])))
+
+
+def read_cloud_ply(path: str):
+    """read_cloud_ply (ply_io.hpp:193-221): (positions, normals, colors)."""
+    n = C.c_int64()
+    _check(lib().dsg_cloud_load_ply(os.fsencode(path), None, None, None, C.c_int64(0), C.byref(n)))
+    out = [np.zeros((n.value, 3)) for _ in range(3)]
+    _check(lib().dsg_cloud_load_ply(os.fsencode(path), *[_p(a) for a in out], C.c_int64(n.value),
+                                    C.byref(n)))
+    return tuple(out)
+
+
+def image_metrics(a, b, ctx: Context = None):
+    """(psnr, ssim) of two (h, w, 3) images (metrics.hpp:20-38) on the device."""
+    ctx = ctx or default_context()
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    if a.shape != b.shape or a.ndim != 3 or a.shape[2] != 3:
+        raise DsplatError(ErrorCode.DimensionMismatch, "image shapes differ")
+    ps, ss = C.c_double(), C.c_double()
+    _check(lib().dsg_image_metrics(ctx.h, _p(a), _p(b), C.c_int32(a.shape[1]),
+                                   C.c_int32(a.shape[0]), C.byref(ps), C.byref(ss)))
+    return ps.value, ss.value
+
+
+def eval_view(model, truth, cam: Camera, cfg: RenderConfig, ctx: Context = None):
+    """(psnr, ssim) of render(model) vs render(truth) (runtime.hpp:483-492)."""
+    ctx = ctx or default_context()
+    dm, dt = _as_device_model(model, ctx), _as_device_model(truth, ctx)
+    ps, ss = C.c_double(), C.c_double()
+    _check(lib().dsg_eval_view(ctx.h, dm.h, dt.h, C.byref(cam_struct(cam)),
+                               C.byref(cfg_struct(cfg)), C.byref(ps), C.byref(ss)))
+    return ps.value, ss.value

@@ -738,6 +738,85 @@ int dsg_model_download(dsg_ctx ctx, dsg_model model, double* params, int64_t cap
   });
 }
 
+int dsg_model_save_ply(dsg_ctx ctx, dsg_model model, const char* path) {
+  return guarded([&] {  // write_splat_ply (ply_io.hpp:89-119)
+    if (!path) fail(kInvalidArgument, "null path");
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    const int64_t it = m.iteration;
+    const int32_t op = m.origin_partition;
+    const std::string head = ply_header(splat_ply_props(), kParams, m.n, &it, &op);
+    std::vector<char> body((size_t)m.n * kParams * sizeof(double));
+    if (m.n > 0) {
+      double* d = ctx->stage_d.ensure(kParams * m.n);
+      splat_ply_payload_dev(m.params.get(), m.cap, m.n, d, ctx->stream);
+      staged_copy(ctx, body.data(), reinterpret_cast<char*>(d), body.size(), true);
+    }
+    write_file_atomic(path, head, body.data(), body.size());
+  });
+}
+
+int dsg_model_load_ply(dsg_ctx ctx, dsg_model model, const char* path) {
+  return guarded([&] {  // read_splat_ply (ply_io.hpp:121-158); resets the optimizer like upload
+    if (!path) fail(kInvalidArgument, "null path");
+    const std::string bytes = read_file(path);
+    const PlyInfo h = parse_ply(bytes, splat_ply_props(), kParams, "splat");
+    DeviceGuard g(ctx->device);
+    ModelDev& m = model->m;
+    m.reserve(std::max<int64_t>(h.vertex_count, 1));
+    m.n = h.vertex_count;
+    m.iteration = h.iteration;
+    m.origin_partition = h.origin;
+    if (m.n > 0) {
+      double* d = ctx->stage_d.ensure(kParams * m.n);
+      staged_copy(ctx, const_cast<char*>(bytes.data()) + h.payload_offset,
+                  reinterpret_cast<char*>(d), (size_t)m.n * kParams * sizeof(double), false);
+      splat_ply_scatter_dev(d, m.n, m.params.get(), m.cap, ctx->stream);
+    }
+    reset_optimizer(ctx, m);
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int dsg_cloud_save_ply(const char* path, const double* positions, const double* normals,
+                       const double* colors, int64_t n) {
+  return guarded([&] {  // write_cloud_ply (ply_io.hpp:170-191)
+    if (!path || n < 0) fail(kInvalidArgument, "bad cloud arguments");
+    const std::string head = ply_header(cloud_ply_props(), 9, n, nullptr, nullptr);
+    std::vector<double> body(9 * (size_t)n);
+    for (int64_t i = 0; i < n; ++i)
+      for (int c = 0; c < 3; ++c) {
+        body[9 * i + c] = positions[3 * i + c];
+        body[9 * i + 3 + c] = normals ? normals[3 * i + c] : 0.0;
+        body[9 * i + 6 + c] = colors ? colors[3 * i + c] : 0.0;
+      }
+    write_file_atomic(path, head, reinterpret_cast<const char*>(body.data()),
+                      body.size() * sizeof(double));
+  });
+}
+
+int dsg_cloud_load_ply(const char* path, double* positions, double* normals, double* colors,
+                       int64_t capacity, int64_t* n) {
+  return guarded([&] {  // read_cloud_ply (ply_io.hpp:193-221)
+    if (!path || !n) fail(kInvalidArgument, "bad cloud arguments");
+    const std::string bytes = read_file(path);
+    const PlyInfo h = parse_ply(bytes, cloud_ply_props(), 9, "cloud");
+    *n = h.vertex_count;
+    if (!positions) return;  // size query
+    if (capacity < h.vertex_count) fail(kInvalidArgument, "output capacity too small");
+    const double* src = reinterpret_cast<const double*>(bytes.data() + h.payload_offset);
+    std::vector<double> row(9);
+    for (int64_t i = 0; i < h.vertex_count; ++i) {
+      std::memcpy(row.data(), src + 9 * i, sizeof(double) * 9);  // payload may be unaligned
+      for (int c = 0; c < 3; ++c) {
+        positions[3 * i + c] = row[c];
+        if (normals) normals[3 * i + c] = row[3 + c];
+        if (colors) colors[3 * i + c] = row[6 + c];
+      }
+    }
+  });
+}
+
 int dsg_model_info(dsg_model model, int64_t* n, int64_t* iteration, int64_t* adam_step) {
   return guarded([&] {
     if (n) *n = model->m.n;
@@ -1479,6 +1558,16 @@ int dsg_nvtx_pop(void) {
   return 0;
 }
 
+int dsg_frame_work(dsg_ctx ctx, int64_t* composited, int64_t* term_fixups) {
+  return guarded([&] {
+    DeviceGuard g(ctx->device);
+    int64_t c = 0, f = 0;
+    frame_work_dev(ctx->frame, ctx->stream, &c, &f);
+    if (composited) *composited = c;
+    if (term_fixups) *term_fixups = f;
+  });
+}
+
 int dsg_frame_stats(dsg_ctx ctx, int64_t* n_visible, int64_t* n_dup) {
   return guarded([&] {
     if (n_visible) *n_visible = ctx->frame.n_visible;
@@ -1506,6 +1595,57 @@ int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32
     cudaEventDestroy(a);
     cudaEventDestroy(b);
     *ms = t;
+  });
+}
+
+int dsg_image_metrics(dsg_ctx ctx, const double* a, const double* b, int32_t width,
+                      int32_t height, double* psnr, double* ssim) {
+  return guarded([&] {  // psnr / ssim (metrics.hpp:20-38) of two HWC double RGB images
+    if (!a || !b || width <= 0 || height <= 0) fail(kDimensionMismatch, "image shapes differ");
+    if (ssim && (width < 11 || height < 11))
+      fail(kTooSmall, "images must be at least 11 px per side");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t npix = (int64_t)width * height;
+    double* d = ctx->stage_d.ensure(6 * npix);
+    float* f = ctx->stage_f.ensure(6 * npix);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d, a, sizeof(double) * 3 * npix, cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(d + 3 * npix, b, sizeof(double) * 3 * npix,
+                                   cudaMemcpyHostToDevice, st));
+    k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d, npix, 3, f, npix);
+    k_aos_to_planar<<<nblk(npix), 256, 0, st>>>(d + 3 * npix, npix, 3, f + 3 * npix, npix);
+    count_launch(2);
+    double* out = ctx->frame.loss_out.ensure(2);
+    image_metrics_dev(ctx->frame, f, f + 3 * npix, width, height, st, out);
+    double h[2];
+    DSG_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (psnr) *psnr = h[0];
+    if (ssim) *ssim = h[1];
+  });
+}
+
+int dsg_eval_view(dsg_ctx ctx, dsg_model model, dsg_model truth, const dsg_camera* cam_in,
+                  const dsg_render_config* cfg, double* psnr, double* ssim) {
+  return guarded([&] {  // runtime.hpp:483-492: psnr/ssim of render(merged) vs render(gt)
+    RenderDev rd = make_rd(cfg);
+    CamDev cam = make_cam(cam_in);
+    if (cam.width < 11 || cam.height < 11) fail(kTooSmall, "images must be at least 11 px per side");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    const int64_t npix = (int64_t)cam.width * cam.height;
+    forward(ctx, truth->m, cam, rd);
+    float* t = ctx->stage_f.ensure(3 * npix);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(t, ctx->frame.rgb.get(), sizeof(float) * 3 * npix,
+                                   cudaMemcpyDeviceToDevice, st));
+    forward(ctx, model->m, cam, rd);
+    double* out = ctx->frame.loss_out.ensure(2);
+    image_metrics_dev(ctx->frame, ctx->frame.rgb.get(), t, cam.width, cam.height, st, out);
+    double h[2];
+    DSG_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof h, cudaMemcpyDeviceToHost, st));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (psnr) *psnr = h[0];
+    if (ssim) *ssim = h[1];
   });
 }
 

@@ -149,6 +149,7 @@ struct AlphaEval {
   float om;      // 1 - alpha, formed so the 0.999 clamp gives exactly 1e-3
   float g;       // gaussian value
   bool gate;     // o*g <= 0.999 (gradient flows through the clamp)
+  float err;     // bound on alpha's relative error (forward's termination bound)
 };
 
 }  // namespace dsg

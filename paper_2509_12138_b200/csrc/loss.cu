@@ -254,6 +254,42 @@ __global__ void __launch_bounds__(256) k_loss_final(LossArgs a) {
   }
 }
 
+// Squared error per block (psnr, metrics.hpp:20-30), fp64, deterministic.
+__global__ void __launch_bounds__(kB* kB) k_sq_err(LossArgs a) {
+  __shared__ double red[32];
+  const int cx = blockIdx.x * kB + threadIdx.x % kB, cy = blockIdx.y * kB + threadIdx.x / kB;
+  double e = 0.0;
+  if (cx < a.w && cy < a.h) {
+    const int64_t o = (int64_t)cy * a.w + cx;
+    for (int ch = 0; ch < 3; ++ch) {
+      const double d = (double)a.x[ch * a.npix + o] - (double)a.y[ch * a.npix + o];
+      e += d * d;
+    }
+  }
+  const double t = block_sum_d(e, red);
+  if (threadIdx.x == 0) a.parts[a.nblocks + blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
+// out[0] = psnr (kPsnrCap 99 when identical), out[1] = mean windowed SSIM
+// over the valid centres (metrics.hpp:20-38, ssim.hpp:48-121)
+__global__ void __launch_bounds__(256) k_metric_final(LossArgs a) {
+  __shared__ double red[32];
+  double s = 0.0, l = 0.0;
+  for (int i = threadIdx.x; i < a.nblocks; i += blockDim.x) {
+    s += a.parts[i];
+    l += a.parts[a.nblocks + i];
+  }
+  const double ss = block_sum_d(s, red);
+  __syncthreads();
+  const double se = block_sum_d(l, red);
+  if (threadIdx.x == 0) {
+    const double mse = se / (double)(3 * a.npix);
+    a.loss_out[0] = mse <= 0.0 ? 99.0 : fmin(99.0, 10.0 * log10(1.0 / mse));
+    const uint32_t nc = a.counts[1];
+    a.loss_out[1] = nc ? ss / ((double)nc * 3.0) : 0.0;
+  }
+}
+
 // gaussian_window (ssim.hpp:17-31) factored: g_k / sum(g), sigma 1.5
 void fill_window(double* g) {
   double sum = 0.0;
@@ -299,6 +335,39 @@ void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, 
   count_launch();
   k_loss_final<<<1, 256, 0, st>>>(a);
   count_launch();
+  DSG_CUDA_CHECK(cudaGetLastError());
+}
+
+// psnr and ssim (metrics.hpp:20-38) of two planar fp32 RGB images on the
+// device; out (device) receives {psnr, ssim}.
+void image_metrics_dev(Frame& f, const float* x, const float* y, int width, int height,
+                       cudaStream_t st, double* out) {
+  const int64_t npix = (int64_t)width * height;
+  dim3 grid((width + kB - 1) / kB, (height + kB - 1) / kB);
+  const int nblocks = grid.x * grid.y;
+  f.ssim_pqr.ensure(9 * npix);
+  f.loss_parts.ensure(2 * nblocks);
+  f.loss_counts.ensure(2);
+  uint8_t* ones = f.ones_mask.ensure(npix);
+  DSG_CUDA_CHECK(cudaMemsetAsync(ones, 1, npix, st));
+  DSG_CUDA_CHECK(cudaMemsetAsync(f.loss_counts.get(), 0, 2 * sizeof(uint32_t), st));
+  LossArgs a{};
+  a.x = x;
+  a.y = y;
+  a.m = ones;
+  a.w = width;
+  a.h = height;
+  a.npix = npix;
+  a.pqr = f.ssim_pqr.get();
+  a.parts = f.loss_parts.get();
+  a.counts = f.loss_counts.get();
+  a.loss_out = out;
+  a.nblocks = nblocks;
+  fill_window(a.win);
+  k_ssim_stats<<<grid, kB * kB, 0, st>>>(a);
+  k_sq_err<<<grid, kB * kB, 0, st>>>(a);
+  k_metric_final<<<1, 256, 0, st>>>(a);
+  count_launch(3);
   DSG_CUDA_CHECK(cudaGetLastError());
 }
 

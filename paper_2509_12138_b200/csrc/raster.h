@@ -77,6 +77,7 @@ struct Frame {
   int64_t unit_cap = 0, band_tiles = 0, seg_len = kSegMin, split_len = 0, split_cap = 0;
   DevBuf<uint32_t> counters;
   DevBuf<uint32_t> amb, tile_unit;  // termination fix-up: flagged pixels, tile -> first unit
+  DevBuf<unsigned long long> work;  // frame_work_dev scratch
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL, Tband;
   DevBuf<uint32_t> last;
@@ -91,6 +92,7 @@ struct Frame {
   DevBuf<double> ssim_pqr, loss_parts;
   DevBuf<uint32_t> loss_counts;
   DevBuf<double> loss_out;
+  DevBuf<uint8_t> ones_mask;  // all-ones mask (unmasked SSIM metric)
   SortScratch sort;
   ScanScratch scan;
   // high-priority side stream for the split-tile forward, which runs beside
@@ -241,5 +243,31 @@ void gather_bands_dev(void* comm, int nranks, int rank, float* rgb, int width, i
                       const std::vector<int>& row0, const std::vector<int>& row1, cudaStream_t st);
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,
                      double lambda, cudaStream_t st, double* out = nullptr);
+
+// sum of n_contrib of the last forward and the termination fix-ups (host values)
+void frame_work_dev(Frame& f, cudaStream_t st, int64_t* composited, int64_t* fixups);
+// psnr / ssim (metrics.hpp:20-38) of planar fp32 RGB images; out = {psnr, ssim} (device)
+void image_metrics_dev(Frame& f, const float* x, const float* y, int width, int height,
+                       cudaStream_t st, double* out);
+
+// float64 PLY (ply_io.hpp:89-221, io.cu)
+struct PlyInfo {
+  int64_t vertex_count = 0;
+  int64_t iteration = 0;
+  int origin = -1;
+  size_t payload_offset = 0;
+};
+std::string ply_header(const char* const* props, int nprops, int64_t n, const int64_t* iteration,
+                       const int32_t* origin);
+void write_file_atomic(const std::string& path, const std::string& head, const char* body,
+                       size_t body_bytes);
+std::string read_file(const std::string& path);
+PlyInfo parse_ply(const std::string& bytes, const char* const* props, int nprops, const char* what);
+void splat_ply_payload_dev(const float* params, int64_t pitch, int64_t n, double* out,
+                           cudaStream_t st);
+void splat_ply_scatter_dev(const double* in, int64_t n, float* params, int64_t pitch,
+                           cudaStream_t st);
+const char* const* splat_ply_props();
+const char* const* cloud_ply_props();
 
 }  // namespace dsg

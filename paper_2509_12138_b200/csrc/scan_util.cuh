@@ -17,8 +17,9 @@ __device__ __forceinline__ T warp_inclusive_sum(T v) {
 }
 
 // Exclusive block-wide sum over NT threads (NT multiple of 32, <= 1024).
-// smem: >= 32 elements. Returns the exclusive prefix; *aggregate = total.
-// Ends with a __syncthreads so smem can be reused.
+// smem: >= 33 elements (per-warp prefixes in [0, 32), the total in [32]).
+// Returns the exclusive prefix; *aggregate = total. Ends with a
+// __syncthreads so smem can be reused.
 template <int NT, class T>
 __device__ __forceinline__ T block_exclusive_sum(T v, T* aggregate, T* smem) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -30,11 +31,11 @@ __device__ __forceinline__ T block_exclusive_sum(T v, T* aggregate, T* smem) {
     T w = lane < NW ? smem[lane] : T(0);
     T wi = warp_inclusive_sum(w);
     if (lane < NW) smem[lane] = wi - w;
-    if (lane == NW - 1) smem[31] = wi;
+    if (lane == NW - 1) smem[32] = wi;  // not [31]: with 32 warps that is warp 31's prefix
   }
   __syncthreads();
   T r = smem[warp] + inc - v;
-  *aggregate = smem[31];
+  *aggregate = smem[32];
   __syncthreads();
   return r;
 }

@@ -110,7 +110,7 @@ scalar:
 
 // Exclusive scan of each pass's 256 bins (one block per pass).
 __global__ void k_hist_scan(uint32_t* ghist) {
-  __shared__ uint32_t tmp[32];
+  __shared__ uint32_t tmp[33];
   uint32_t* h = ghist + blockIdx.x * kRadix;
   uint32_t agg;
   uint32_t ex = block_exclusive_sum<kRadix>(h[threadIdx.x], &agg, tmp);
@@ -125,7 +125,7 @@ struct OnesweepSmem {
   K keys[kPart];
   uint32_t vals[kPart];
   uint32_t part;
-  uint32_t scan[32];
+  uint32_t scan[33];
 };
 
 template <class K>
@@ -250,7 +250,7 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in,
                                                               int64_t n, uint32_t* sums,
                                                               bool flags) {
-  __shared__ uint32_t tmp[32];
+  __shared__ uint32_t tmp[33];
   int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
 #pragma unroll
@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __
 }
 
 __global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, int64_t nb) {
-  __shared__ uint32_t tmp[32];
+  __shared__ uint32_t tmp[33];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __re
                                                             uint32_t* out, int64_t n,
                                                             const uint32_t* __restrict__ sums,
                                                             bool flags) {
-  __shared__ uint32_t tmp[32];
+  __shared__ uint32_t tmp[33];
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
   uint32_t local = 0;
