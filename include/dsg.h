@@ -263,8 +263,18 @@ int dsg_comm_destroy(dsg_comm comm);
  * the survivor exchange (the NCCL broadcast group, 56 B per survivor). */
 int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
                         double cut_hi, dsg_model merged, int64_t* n_merged, double* ms);
+/* The same with several partitions per rank: locals[j] holds partition
+ * k = j * nranks + rank (partition k on GPU k mod N) with its cuts
+ * cut_lo[j], cut_hi[j]; the merged model is in partition order on every rank,
+ * iteration = max over partitions. */
+int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* locals,
+                              int32_t nlocal, int32_t axis, const double* cut_lo,
+                              const double* cut_hi, dsg_model merged, int64_t* n_merged,
+                              double* ms);
 /* Tile-parallel render (comm may be NULL): rank r bins and blends tile-row
- * band r of the replicated model; bands are gathered to rank 0, which
+ * band r of the replicated model, the bands cut at the quantiles of the
+ * splats' projected centres per tile row (computed identically on every
+ * rank); bands are gathered to rank 0, which
  * receives rgb [h][w][3] (may be NULL). *ms = device time incl. the gather. */
 int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const dsg_camera* cam,
                            const dsg_render_config* cfg, double* rgb, double* ms);

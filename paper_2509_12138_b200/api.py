@@ -697,6 +697,21 @@ def merge_allgather(comm: Comm, local: DeviceModel, partition) -> tuple:
     return merged, n.value, ms.value
 
 
+def merge_allgather_multi(comm: Comm, locals_, partitions) -> tuple:
+    """Several partitions per rank: locals_[j] is partition j * nranks + rank
+    (partition k on GPU k mod N); merged model in partition order."""
+    merged = DeviceModel(comm.ctx)
+    n, ms = C.c_int64(), C.c_double()
+    arr = (C.c_void_p * len(locals_))(*[m.h.value if hasattr(m.h, "value") else m.h
+                                        for m in locals_])
+    lo = np.array([p.cut_lo for p in partitions], np.float64)
+    hi = np.array([p.cut_hi for p in partitions], np.float64)
+    _check(lib().dsg_merge_allgather_multi(comm.ctx.h, comm.h, arr, C.c_int32(len(locals_)),
+                                           C.c_int32(partitions[0].cut_axis), _p(lo), _p(hi),
+                                           merged.h, C.byref(n), C.byref(ms)))
+    return merged, n.value, ms.value
+
+
 def render_distributed(comm, model: DeviceModel, cam: Camera, cfg: RenderConfig, want_image=True):
     """Tile-parallel render with the bands gathered to rank 0 (comm may be None)."""
     ctx = model.ctx

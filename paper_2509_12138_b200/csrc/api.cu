@@ -1722,6 +1722,7 @@ int dsg_merge_models(dsg_ctx ctx, const dsg_model* models, int32_t nparts, int32
 struct dsg_comm_s {
   void* nccl = nullptr;
   int nranks = 1, rank = 0;
+  std::vector<int> band_rows;  // first tile row of each rank's band, last distributed render
 };
 
 int dsg_comm_unique_id(uint8_t* out128) {
@@ -1748,29 +1749,33 @@ int dsg_comm_destroy(dsg_comm comm) {
   });
 }
 
-int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
-                        double cut_hi, dsg_model merged, int64_t* n_merged, double* ms) {
+int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* locals,
+                              int32_t nlocal, int32_t axis, const double* cut_lo,
+                              const double* cut_hi, dsg_model merged, int64_t* n_merged,
+                              double* ms) {
   return guarded([&] {
+    if (nlocal < 1 || !locals) fail(kInvalidArgument, "no local partitions");
     DeviceGuard g(ctx->device);
-    cudaEvent_t a, b;
-    DSG_CUDA_CHECK(cudaEventCreate(&a));
-    DSG_CUDA_CHECK(cudaEventCreate(&b));
-    DSG_CUDA_CHECK(cudaEventRecord(a, ctx->stream));
-    float t = 0.f;  // device time of the survivor exchange (NCCL group)
-    int64_t total = merge_allgather_dev(comm->nccl, comm->nranks, comm->rank, local->m, axis,
-                                        cut_lo, cut_hi, merged->m, ctx->frame.scan, ctx->stream,
-                                        &t);
-    DSG_CUDA_CHECK(cudaEventRecord(b, ctx->stream));
-    DSG_CUDA_CHECK(cudaEventSynchronize(b));
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
-    merged->m.iteration = local->m.iteration;
+    std::vector<const ModelDev*> ms_(nlocal);
+    for (int j = 0; j < nlocal; ++j) ms_[j] = &locals[j]->m;
+    float t = 0.f;  // device time of the survivor exchange (the NCCL all-gathers)
+    int64_t it_max = 0;
+    const int64_t total = merge_allgather_dev(comm->nccl, comm->nranks, comm->rank, ms_.data(),
+                                              nlocal, axis, cut_lo, cut_hi, merged->m,
+                                              ctx->frame.scan, ctx->stream, &t, &it_max);
+    merged->m.iteration = it_max;  // merge_models: iteration = max (partition.hpp:124)
     merged->m.origin_partition = -1;
     reset_optimizer(ctx, merged->m);
     DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     if (n_merged) *n_merged = total;
     if (ms) *ms = t;
   });
+}
+
+int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
+                        double cut_hi, dsg_model merged, int64_t* n_merged, double* ms) {
+  return dsg_merge_allgather_multi(ctx, comm, &local, 1, axis, &cut_lo, &cut_hi, merged, n_merged,
+                                   ms);
 }
 
 int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const dsg_camera* cam_in,
@@ -1781,21 +1786,45 @@ int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const ds
     DeviceGuard g(ctx->device);
     cudaStream_t st = ctx->stream;
     const int R = comm ? comm->nranks : 1, me = comm ? comm->rank : 0;
-    // equal bands of tile rows
-    std::vector<int> t0(R), t1(R), r0(R), r1(R);
-    for (int r = 0; r < R; ++r) {
-      t0[r] = (int)((int64_t)cam.tiles_y * r / R);
-      t1[r] = (int)((int64_t)cam.tiles_y * (r + 1) / R);
-      r0[r] = std::min(t0[r] * kTile, cam.height);
-      r1[r] = std::min(t1[r] * kTile, cam.height);
-    }
-    CamDev band = cam;
-    band.band_ty0 = t0[me];
-    band.band_ty1 = t1[me];
     cudaEvent_t a, b;
     DSG_CUDA_CHECK(cudaEventCreate(&a));
     DSG_CUDA_CHECK(cudaEventCreate(&b));
     DSG_CUDA_CHECK(cudaEventRecord(a, st));
+    // Bands of tile rows balanced by splat count: every
+    // rank histograms the replicated model's projected centres per tile row
+    // (integer atomics: identical on every rank, no exchange) and cuts the
+    // rows at the R-quantiles of that count.
+    std::vector<int> t0(R), t1(R), r0(R), r1(R);
+    t0[0] = 0;
+    t1[R - 1] = cam.tiles_y;
+    if (R > 1) {
+      uint32_t* hist = ctx->frame.row_hist.ensure(cam.tiles_y);
+      center_row_hist_dev(model->m.params.get(), model->m.cap, model->m.n, cam, hist, st);
+      std::vector<uint32_t> h(cam.tiles_y);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), hist, sizeof(uint32_t) * cam.tiles_y,
+                                     cudaMemcpyDeviceToHost, st));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+      int64_t total = 0;
+      for (uint32_t v : h) total += v;
+      int64_t run = 0;
+      int row = 0;
+      for (int r = 1; r < R; ++r) {  // first row whose prefix reaches r/R of the splats
+        const int64_t want = total * r / R;
+        while (row < cam.tiles_y && run + h[row] <= want) run += h[row++];
+        // keep every band non-empty and increasing
+        const int lo = t0[r - 1] + 1, hi = cam.tiles_y - (R - r);
+        t0[r] = std::min(std::max(row, lo), hi);
+        t1[r - 1] = t0[r];
+      }
+    }
+    for (int r = 0; r < R; ++r) {
+      r0[r] = std::min(t0[r] * kTile, cam.height);
+      r1[r] = std::min(t1[r] * kTile, cam.height);
+    }
+    if (comm) comm->band_rows.assign(t0.begin(), t0.end());
+    CamDev band = cam;
+    band.band_ty0 = t0[me];
+    band.band_ty1 = t1[me];
     forward(ctx, model->m, band, rd);
     if (R > 1) gather_bands_dev(comm->nccl, R, me, ctx->frame.rgb.get(), cam.width, cam.height, r0, r1, st);
     DSG_CUDA_CHECK(cudaEventRecord(b, st));

@@ -453,7 +453,44 @@ __global__ void k_tile_order(const uint32_t* __restrict__ bins, int t0, int nt, 
 
 inline unsigned blocks(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// Splats per tile row by projected centre (fp32; only balances the bands of
+// the tile-parallel render, never decides a pixel). Block histograms in
+// shared memory, then one global atomic per non-empty row.
+__global__ void k_center_rows(const float* __restrict__ P, int64_t pitch, int64_t n, CamDev cam,
+                              uint32_t* __restrict__ hist) {
+  extern __shared__ uint32_t h[];
+  for (int t = threadIdx.x; t < cam.tiles_y; t += blockDim.x) h[t] = 0;
+  __syncthreads();
+  const float R0 = (float)cam.R[0], R1 = (float)cam.R[1], R2 = (float)cam.R[2];
+  const float R3 = (float)cam.R[3], R4 = (float)cam.R[4], R5 = (float)cam.R[5];
+  const float R6 = (float)cam.R[6], R7 = (float)cam.R[7], R8 = (float)cam.R[8];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float x = P[i] - (float)cam.pos[0], y = P[pitch + i] - (float)cam.pos[1],
+                z = P[2 * pitch + i] - (float)cam.pos[2];
+    const float tz = R6 * x + R7 * y + R8 * z;
+    if (!(tz > (float)cam.near_plane)) continue;
+    const float tx = R0 * x + R1 * y + R2 * z, ty = R3 * x + R4 * y + R5 * z;
+    const float u = (float)cam.half_w + (float)cam.f * tx / tz;
+    const float v = (float)cam.half_h - (float)cam.f * ty / tz;
+    if (u < 0.f || u >= (float)cam.width || v < 0.f || v >= (float)cam.height) continue;
+    atomicAdd(&h[min((int)v / kTile, cam.tiles_y - 1)], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < cam.tiles_y; t += blockDim.x)
+    if (h[t]) atomicAdd(&hist[t], h[t]);
+}
+
 }  // namespace
+
+void center_row_hist_dev(const float* params, int64_t pitch, int64_t n, const CamDev& cam,
+                         uint32_t* hist, cudaStream_t st) {
+  DSG_CUDA_CHECK(cudaMemsetAsync(hist, 0, sizeof(uint32_t) * cam.tiles_y, st));
+  if (n <= 0) return;
+  const unsigned g = (unsigned)std::min<int64_t>(blocks(n, 256), 148 * 8);
+  k_center_rows<<<g, 256, sizeof(uint32_t) * cam.tiles_y, st>>>(params, pitch, n, cam, hist);
+  count_launch();
+}
 
 std::atomic<int> g_exact_masks{1};
 

@@ -5,8 +5,9 @@
 //   1. each rank compacts the splats its partition owns (merge_models keep
 //      rule, partition.hpp:120) on the device;
 //   2. the survivor counts are all-gathered (int64);
-//   3. the survivors are broadcast from every rank into one merged planar
-//      model in (partition, index) order — merge_models' order
+//   3. the survivors are all-gathered as packed 56 B records (one NCCL
+//      all-gather, padded to the largest slab) and scattered into one merged
+//      planar model in (partition, index) order — merge_models' order
 //      (partition.hpp:117-123) — so every GPU holds the merged model;
 //   4. the merged model is rendered tile-parallel: rank r bins and blends
 //      only its band of tile rows (preprocess is replicated), and the bands
@@ -108,55 +109,121 @@ void nccl_comm_destroy(void* c) {
   if (c) nccl().CommDestroy((ncclComm_t)c);
 }
 
+namespace {
+// survivors, planar [14][pitch] -> packed records [cnt][14] (56 B per splat)
+__global__ void k_pack_records(const float* __restrict__ dense, int64_t pitch, int64_t cnt,
+                               float* __restrict__ rec) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= cnt * kParams) return;
+  const int64_t i = t / kParams;
+  const int k = (int)(t - i * kParams);
+  rec[t] = dense[k * pitch + i];
+}
+// the gathered [R][maxc][14] records -> merged planar model, rank r's
+// survivors at offset off[r] (merge_models' (partition, index) order)
+__global__ void k_unpack_records(const float* __restrict__ rec, int64_t maxc, int nranks,
+                                 const int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                                 float* __restrict__ P, int64_t pitch) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)nranks * maxc * kParams) return;
+  const int64_t row = t / kParams;
+  const int k = (int)(t - row * kParams);
+  const int r = (int)(row / maxc);
+  const int64_t i = row - (int64_t)r * maxc;
+  if (i >= cnt[r]) return;  // padding
+  P[k * pitch + off[r] + i] = rec[t];
+}
+}  // namespace
+
 // Steps 1-3 above. `merged` receives the merged model (reserved inside).
-int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& local, int axis,
-                            double cut_lo, double cut_hi, ModelDev& merged, ScanScratch& sc,
-                            cudaStream_t st, float* wire_ms) {
+// Rank r holds partitions k = j * nranks + r for j < nlocal (partition k on
+// GPU k mod N, runtime.hpp:337-343 worker assignment). The survivors travel
+// as packed 56 B records: one NCCL all-gather per round j, every rank's
+// records padded to that round's largest count (slabs are count-balanced, so
+// the padding is the ghost imbalance); one kernel per round scatters them
+// into the merged planar store at their (partition, index) offsets.
+int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* const* locals,
+                            int nlocal, int axis, const double* cut_lo, const double* cut_hi,
+                            ModelDev& merged, ScanScratch& sc, cudaStream_t st, float* wire_ms,
+                            int64_t* max_iteration) {
   Nccl& N = nccl();
   ncclComm_t c = (ncclComm_t)comm;
-  // 1. local compaction into a dense [14][cnt] buffer
-  int64_t cnt = merge_compact_dev(local.params.get(), local.cap, local.n, axis, cut_lo, cut_hi,
-                                  nullptr, 0, 0, sc, st);
-  DevBuf<float> dense;
-  dense.ensure((size_t)kParams * std::max<int64_t>(cnt, 1));
-  merge_compact_dev(local.params.get(), local.cap, local.n, axis, cut_lo, cut_hi, dense.get(),
-                    std::max<int64_t>(cnt, 1), 0, sc, st);
-  // 2. counts
-  DevBuf<int64_t> counts;
-  counts.ensure(nranks + 1);
-  DSG_CUDA_CHECK(cudaMemcpyAsync(counts.get() + nranks, &cnt, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  nc(N.AllGather(counts.get() + nranks, counts.get(), 1, ncclInt64, c, st), "allgather counts");
-  std::vector<int64_t> hc(nranks);
-  DSG_CUDA_CHECK(cudaMemcpyAsync(hc.data(), counts.get(), sizeof(int64_t) * nranks, cudaMemcpyDeviceToHost, st));
-  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-  int64_t total = 0;
-  std::vector<int64_t> off(nranks);
-  for (int r = 0; r < nranks; ++r) {
-    off[r] = total;
-    total += hc[r];
+  const int P = nranks * nlocal;
+  // 1. local compaction of each partition into a dense [14][cnt] buffer
+  std::vector<int64_t> mine(2 * nlocal);
+  std::vector<DevBuf<float>> dense(nlocal);
+  for (int j = 0; j < nlocal; ++j) {
+    const ModelDev& L = *locals[j];
+    const int64_t cnt = merge_compact_dev(L.params.get(), L.cap, L.n, axis, cut_lo[j], cut_hi[j],
+                                          nullptr, 0, 0, sc, st);
+    dense[j].ensure((size_t)kParams * std::max<int64_t>(cnt, 1));
+    merge_compact_dev(L.params.get(), L.cap, L.n, axis, cut_lo[j], cut_hi[j], dense[j].get(),
+                      std::max<int64_t>(cnt, 1), 0, sc, st);
+    mine[2 * j] = cnt;
+    mine[2 * j + 1] = L.iteration;
   }
-  // 3. every rank's survivors, broadcast row by row into the merged model
+  // 2. (count, iteration) of every partition
+  DevBuf<int64_t> meta;
+  meta.ensure((size_t)2 * nlocal * (nranks + 1));
+  int64_t* send_meta = meta.get() + (size_t)2 * nlocal * nranks;
+  DSG_CUDA_CHECK(cudaMemcpyAsync(send_meta, mine.data(), sizeof(int64_t) * 2 * nlocal,
+                                 cudaMemcpyHostToDevice, st));
+  nc(N.AllGather(send_meta, meta.get(), (size_t)2 * nlocal, ncclInt64, c, st), "allgather counts");
+  std::vector<int64_t> all((size_t)2 * nlocal * nranks);
+  DSG_CUDA_CHECK(cudaMemcpyAsync(all.data(), meta.get(), sizeof(int64_t) * all.size(),
+                                 cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::vector<int64_t> cnt(P), off(P);
+  int64_t total = 0, it_max = 0;
+  for (int k = 0; k < P; ++k) {  // partition order: merge_models (partition.hpp:117-123)
+    const int r = k % nranks, j = k / nranks;
+    cnt[k] = all[(size_t)r * 2 * nlocal + 2 * j];
+    it_max = std::max(it_max, all[(size_t)r * 2 * nlocal + 2 * j + 1]);
+    off[k] = total;
+    total += cnt[k];
+  }
+  if (max_iteration) *max_iteration = it_max;
+  // per round: counts and offsets of partitions j * N + r, r = 0..N-1
+  DevBuf<int64_t> co;
+  co.ensure((size_t)2 * P);
+  DSG_CUDA_CHECK(cudaMemcpyAsync(co.get(), cnt.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
+  DSG_CUDA_CHECK(cudaMemcpyAsync(co.get() + P, off.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
   merged.reserve(std::max<int64_t>(total, 1));
   merged.n = total;
+  // 3. pack, all-gather, unpack, round by round
+  int64_t maxc_all = 1;
+  for (int k = 0; k < P; ++k) maxc_all = std::max(maxc_all, cnt[k]);
+  DevBuf<float> send, recv;
+  send.ensure((size_t)maxc_all * kParams);
+  recv.ensure((size_t)nranks * maxc_all * kParams);
   cudaEvent_t e0, e1;
   DSG_CUDA_CHECK(cudaEventCreate(&e0));
   DSG_CUDA_CHECK(cudaEventCreate(&e1));
-  DSG_CUDA_CHECK(cudaEventRecord(e0, st));
-  nc(N.GroupStart(), "group start");
-  for (int r = 0; r < nranks; ++r) {
-    if (hc[r] == 0) continue;
-    for (int k = 0; k < kParams; ++k) {
-      const float* send = r == rank ? dense.get() + (size_t)k * std::max<int64_t>(cnt, 1) : nullptr;
-      nc(N.Broadcast(send, merged.params.get() + (size_t)k * merged.cap + off[r], (size_t)hc[r],
-                     ncclFloat32, r, c, st),
-         "broadcast survivors");
-    }
-  }
-  nc(N.GroupEnd(), "group end");
-  DSG_CUDA_CHECK(cudaEventRecord(e1, st));
-  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
   float t = 0.f;
-  DSG_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+  for (int j = 0; j < nlocal; ++j) {
+    int64_t maxc = 1;
+    for (int r = 0; r < nranks; ++r) maxc = std::max(maxc, cnt[j * nranks + r]);
+    const int64_t my = cnt[j * nranks + rank];
+    if (my > 0) {
+      k_pack_records<<<(unsigned)((my * kParams + 255) / 256), 256, 0, st>>>(
+          dense[j].get(), std::max<int64_t>(my, 1), my, send.get());
+      count_launch();
+    }
+    DSG_CUDA_CHECK(cudaEventRecord(e0, st));
+    nc(N.AllGather(send.get(), recv.get(), (size_t)maxc * kParams, ncclFloat32, c, st),
+       "allgather survivors");
+    DSG_CUDA_CHECK(cudaEventRecord(e1, st));
+    const int64_t tot_rec = (int64_t)nranks * maxc * kParams;
+    k_unpack_records<<<(unsigned)((tot_rec + 255) / 256), 256, 0, st>>>(
+        recv.get(), maxc, nranks, co.get() + (size_t)j * nranks, co.get() + P + (size_t)j * nranks,
+        merged.params.get(), merged.cap);
+    count_launch();
+    DSG_CUDA_CHECK(cudaEventSynchronize(e1));
+    float tj = 0.f;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&tj, e0, e1));
+    t += tj;
+  }
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (wire_ms) *wire_ms = t;

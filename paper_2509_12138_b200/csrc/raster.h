@@ -78,6 +78,7 @@ struct Frame {
   DevBuf<uint32_t> counters;
   DevBuf<uint32_t> amb, tile_unit;  // termination fix-up: flagged pixels, tile -> first unit
   DevBuf<unsigned long long> work;  // frame_work_dev scratch
+  DevBuf<uint32_t> row_hist;        // splats per tile row (render band balancing)
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL, Tband;
   DevBuf<uint32_t> last;
@@ -181,6 +182,9 @@ struct StageTimer {
 extern std::atomic<int> g_exact_masks;
 void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const CamDev& cam,
                const RenderDev& rd, cudaStream_t st, StageTimer* timer = nullptr);
+// per tile row: splats whose projected centre falls in it (band balancing)
+void center_row_hist_dev(const float* params, int64_t pitch, int64_t n, const CamDev& cam,
+                         uint32_t* hist, cudaStream_t st);
 void blend_forward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,
                    const RenderDev& rd, cudaStream_t st);
 void blend_backward(Frame& f, const float* params, int64_t pitch, const CamDev& cam,
@@ -236,9 +240,10 @@ DensifyResult densify_dev(ModelDev& m, ModelDev& spare, DensifyScratch& ds, doub
 void nccl_unique_id(uint8_t out[128]);
 void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(void* comm);
-int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev& local, int axis,
-                            double cut_lo, double cut_hi, ModelDev& merged, ScanScratch& sc,
-                            cudaStream_t st, float* wire_ms = nullptr);
+int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* const* locals,
+                            int nlocal, int axis, const double* cut_lo, const double* cut_hi,
+                            ModelDev& merged, ScanScratch& sc, cudaStream_t st,
+                            float* wire_ms = nullptr, int64_t* max_iteration = nullptr);
 void gather_bands_dev(void* comm, int nranks, int rank, float* rgb, int width, int height,
                       const std::vector<int>& row0, const std::vector<int>& row1, cudaStream_t st);
 void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, int height,

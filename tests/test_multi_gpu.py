@@ -50,6 +50,52 @@ if rank == 0:
     single = api.render(api.DeviceModel(ctx, ref), cam, RenderConfig(), ctx=ctx).color
     assert np.array_equal(img, single), np.max(np.abs(img - single))
     print("MULTI_GPU_OK", n, ms, rms)
+
+# at scale: a Kingsnake cloud in `world` slabs with device seeds, merged with
+# the packed all-gather and rendered at 3840x2160 in count-balanced bands
+from paper_2509_12138_b200 import scenes
+from paper_2509_12138_b200.types import Camera
+pts, cols, _ = scenes.kingsnake(600_000, seed=3)
+parts = api.partition_cloud(pts, world, 0.002, ctx=ctx)
+idx = np.concatenate([parts[rank].owned_indices, parts[rank].ghost_indices]).astype(np.int64)
+seeds = api.seed_gaussians(np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx]), 3, ctx=ctx)
+host = seeds.download()
+host.origin_partition = rank
+merged, n, ms = api.merge_allgather(comm, seeds, parts[rank])
+allp = [None] * world
+dist.all_gather_object(allp, host.params)
+c = (pts.min(0) + pts.max(0)) * 0.5
+cam4k = Camera((float(c[0]) + 1.2, float(c[1]) + 0.4, float(c[2]) - 1.5), tuple(float(v) for v in c),
+               (0.0, 1.0, 0.0), 0.9, 3840, 2160, 0.05, 50.0)
+img, rms = api.render_distributed(comm, merged, cam4k, RenderConfig())
+if rank == 0:
+    from host_partition import merge_models
+    ref = merge_models([SplatModel(p, 0, k) for k, p in enumerate(allp)], parts)
+    assert np.array_equal(merged.download().params, ref.params), "merged model differs (scale)"
+    single = api.render(api.DeviceModel(ctx, ref), cam4k, RenderConfig(), ctx=ctx).color
+    assert np.array_equal(img, single), np.max(np.abs(img - single))
+    print("MULTI_GPU_SCALE_OK", n, ms, rms)
+
+# two partitions per rank (partition k on GPU k mod N): the multi-partition
+# exchange returns merge_models' (partition, index) order
+P = 2 * world
+parts = api.partition_cloud(pts, P, 0.002, ctx=ctx)
+mine = [rank, rank + world]
+locs, hosts = [], {}
+for k in mine:
+    idx = np.concatenate([parts[k].owned_indices, parts[k].ghost_indices]).astype(np.int64)
+    dmk = api.seed_gaussians(np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx]), 3, ctx=ctx)
+    locs.append(dmk)
+    hosts[k] = dmk.download().params
+merged, n, ms = api.merge_allgather_multi(comm, locs, [parts[k] for k in mine])
+allh = [None] * world
+dist.all_gather_object(allh, hosts)
+if rank == 0:
+    from host_partition import merge_models
+    byk = {k: v for d in allh for k, v in d.items()}
+    ref = merge_models([SplatModel(byk[k], 0, k) for k in range(P)], parts)
+    assert np.array_equal(merged.download().params, ref.params), "multi-partition merge differs"
+    print("MULTI_GPU_MULTI_OK", n, ms)
 comm.close()
 dist.barrier()
 dist.destroy_process_group()
@@ -64,9 +110,10 @@ def _ngpus():
         return 0
 
 
-def test_merge_allgather_and_band_render_2gpu(tmp_path):
-    if _ngpus() < 2:
-        pytest.skip("needs >= 2 GPUs")
+@pytest.mark.parametrize("world", [2, 4])
+def test_merge_allgather_and_band_render(tmp_path, world):
+    if _ngpus() < world:
+        pytest.skip(f"needs >= {world} GPUs")
     script = tmp_path / "worker.py"
     script.write_text(WORKER)
     s = socket.socket()
@@ -75,6 +122,10 @@ def test_merge_allgather_and_band_render_2gpu(tmp_path):
     s.close()
     env = dict(os.environ, ROOT=ROOT)
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        "--nproc-per-node", str(world), "--master-addr", "127.0.0.1", "--master-port",
                         str(port), str(script)], capture_output=True, text=True, timeout=600, env=env)
-    assert r.returncode == 0 and "MULTI_GPU_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.returncode == 0 and "MULTI_GPU_MULTI_OK" in r.stdout, r.stdout[-3000:] + r.stderr[-3000:]
+    log = os.path.join(ROOT, "gpurun_out", f"multi_gpu_{world}.log")
+    os.makedirs(os.path.dirname(log), exist_ok=True)
+    with open(log, "w") as f:
+        f.write(r.stdout)
