@@ -254,21 +254,36 @@ KERNEL_OF_STAGE = {"preprocess": "k_preprocess", "depth_sort": "k_onesweep (dept
 
 
 def algorithmic_bytes(stage: str, n: int, nv: int, npix: int, n_dup: int) -> float:
-    """Minimal HBM bytes one launch must move (DESIGN.md section 4)."""
+    """Minimal HBM bytes one launch must move (SURVEY §8d; DESIGN.md §3)."""
     return {
-        "preprocess": 56.0 * n + 4.0 * n + 104.0 * nv,     # params in; count; payload+rect+depth+key out
+        "preprocess": 92.0 * n,                             # §8d: 56 B params in + 36 B out per G
         "depth_sort": 4 * 16.0 * nv + 8.0 * nv,            # 4 passes (32-bit key) x (key,val) r+w + histogram read
-        "scan_duplicate": 64.0 * nv + 8.0 * n_dup,         # counts, scan, rects + mask constants in, (tile|mask, idx) out
+        "scan_duplicate": 8.0 * nv + 16.0 * nv + 8.0 * n_dup,  # §8d scan + duplicate; 8 B (tile|mask, idx) per dup
         "tile_sort_ranges": 2 * 16.0 * n_dup + 9.0 * n_dup,  # 2 passes, ranges + sub-tile masks
         "blend_fwd": 5.0 * n_dup + 48.0 * n_dup + 20.0 * npix,   # list + payload per entry, pixel out
-        "loss": 37.0 * npix,
+        "loss": 37.0 * npix,                                # §8d
         "blend_bwd": 5.0 * n_dup + 68.0 * n_dup + 20.0 * npix + 36.0 * n_dup,  # + >=1 partial/entry
         "chain": 112.0 * n + 36.0 * n_dup + 4.0 * n_dup,   # params+grads, partials, masks
-        "adam": 412.0 * n,                                  # p,g,m,v in; p,m,v out; stats
+        "adam": 412.0 * n,                                  # §8d 392 B/G + 20 B/G fused stats
     }[stage]
 
 
-def roofline(stage_ms, n, nv, npix, n_dup, peak, peak_kind):
+ISSUE_BOUND = ("blend_fwd", "blend_bwd")
+
+
+def roofline(stage_ms, n, nv, npix, n_dup, peak, peak_kind, sm_mhz=None, work=None):
+    """Per-stage HBM fractions, and the dominant kernel's roofline. The blend
+    kernels are bound by instruction issue, not HBM (DRAM is 3-7% busy under
+    ncu): their roofline is warp instructions issued per second (ncu's count
+    per launch over the live launch time) against 148 SMs x 4 schedulers x
+    the SM clock, with the §8d work rate (composited pairs C per second
+    against 148 x 128 FP32 lanes x clock) beside it."""
+    traffic = {}
+    try:
+        with open(TRAFFIC_PATH) as f:
+            traffic = json.load(f)
+    except (OSError, ValueError):
+        pass
     rows = {}
     for st, ms in stage_ms.items():
         if ms <= 0:
@@ -276,26 +291,44 @@ def roofline(stage_ms, n, nv, npix, n_dup, peak, peak_kind):
         b = algorithmic_bytes(st, n, nv, npix, n_dup)
         gbs = b / (ms * 1e-3) / 1e9
         rows[st] = {"ms": round(ms, 4), "GB/s": round(gbs, 1), "frac": round(gbs / peak, 4)}
+    clk = (sm_mhz or 1965.0) * 1e6
+    issue_peak = 148 * 4 * clk
+    lane_peak = 148 * 128 * clk
+    for st in ISSUE_BOUND:
+        tr = traffic.get(KERNEL_OF_STAGE[st], {})
+        if st in rows and tr.get("warp_inst_per_launch"):
+            ips = float(tr["warp_inst_per_launch"]) / (stage_ms[st] * 1e-3)
+            rows[st]["issue_frac"] = round(ips / issue_peak, 4)
+        if st in rows and work and work.get("composited"):
+            rows[st]["pairs_per_s"] = round(work["composited"] / (stage_ms[st] * 1e-3), 1)
+            rows[st]["pair_lane_frac"] = round(work["composited"] / (stage_ms[st] * 1e-3) / lane_peak, 5)
     dom = max(stage_ms, key=stage_ms.get)
+    kern = KERNEL_OF_STAGE[dom]
+    tr = traffic.get(kern, {})
     d = rows[dom]
-    out = {"bound": "hbm", "kernel": KERNEL_OF_STAGE[dom], "achieved": d["GB/s"], "peak": peak,
-           "unit": "GB/s", "frac": d["frac"],
-           "bytes_per_launch": algorithmic_bytes(dom, n, nv, npix, n_dup), "traffic": None,
-           "peak_kind": peak_kind, "per_stage": rows}
-    # dram read+write per launch of the same kernel from the committed ncu --set full capture
-    try:
-        with open(TRAFFIC_PATH) as f:
-            tr = json.load(f).get(KERNEL_OF_STAGE[dom])
-        if tr:
-            out["traffic"] = float(tr["dram_bytes_per_launch"])
-            out["traffic_source"] = tr["source"]
-            if "issue_active_pct" in tr:  # the bound that applies to the blend kernels
-                out["issue_slots_busy_frac"] = round(float(tr["issue_active_pct"]) / 100.0, 3)
-    except (OSError, ValueError, KeyError):
-        pass
-    if dom in ("blend_fwd", "blend_bwd"):
-        out["note"] = ("dominant kernel is the per-pixel blend: FP32/issue- and latency-bound, "
-                       "not HBM-bound; see profiles/ for issue-slot and stall data")
+    if dom in ISSUE_BOUND and tr.get("warp_inst_per_launch"):
+        ips = float(tr["warp_inst_per_launch"]) / (stage_ms[dom] * 1e-3)
+        out = {"bound": "issue", "kernel": kern, "achieved": round(ips / 1e9, 2), "peak": round(issue_peak / 1e9, 2),
+               "unit": "G warp-inst/s", "frac": round(ips / issue_peak, 4),
+               "peak_basis": f"148 SMs x 4 issue slots x {clk / 1e6:.0f} MHz (SM clock under load)",
+               "inst_per_launch": float(tr["warp_inst_per_launch"]),
+               "ncu_issue_active_pct": tr.get("issue_active_pct"),
+               "ncu_fma_pipe_pct": tr.get("fma_pipe_pct"), "ncu_xu_pipe_pct": tr.get("xu_pipe_pct")}
+        if work and work.get("composited"):
+            out["work"] = {"composited_pairs": work["composited"],
+                           "pairs_per_s": d.get("pairs_per_s"),
+                           "lane_peak_per_s": round(lane_peak, 1),
+                           "frac": d.get("pair_lane_frac"),
+                           "model": "§8d: ~40 FP32 ops + 1 MUFU per composited pair (backward)"}
+        out["hbm"] = {"achieved_GBps": d["GB/s"], "peak_GBps": peak, "frac": d["frac"],
+                      "bytes_per_launch": algorithmic_bytes(dom, n, nv, npix, n_dup)}
+    else:
+        out = {"bound": "hbm", "kernel": kern, "achieved": d["GB/s"], "peak": peak, "unit": "GB/s",
+               "frac": d["frac"], "bytes_per_launch": algorithmic_bytes(dom, n, nv, npix, n_dup)}
+    out["traffic"] = float(tr["dram_bytes_per_launch"]) if tr.get("dram_bytes_per_launch") else None
+    out["traffic_source"] = tr.get("source")
+    out["peak_kind"] = peak_kind
+    out["per_stage"] = rows
     return out
 
 
@@ -311,31 +344,69 @@ def run_partitioned(args, dist: Dist):
     """BASELINE configs[2]/[3] shape: a fixed cloud cut into P partitions
     (P >= GPUs), partition k trained on GPU k mod N (runtime.hpp:337-343
     worker assignment). One step = one iteration of one partition; value =
-    all partitions' iterations / the slowest rank's device time."""
+    all partitions' iterations / the slowest rank's device time (strong
+    scaling: the job is fixed, N GPUs share it).
+
+    Views: every partition has its own GT renders and masks of the global
+    rig (runtime.hpp:190-232). At 2048^2 all 403 views of 8 partitions are
+    176 GB, more than one GPU holds beside the models, so with --stream-views
+    (automatic when the views would not fit) only the views the schedule
+    touches are rendered, kept in pinned host memory and streamed one per
+    step (dsg_views_create_host, overlapped with the previous step).
+
+    After the timed steps (--global): the trained partitions are merged —
+    ghost trim + one packed NCCL all-gather per partition round at N > 1,
+    merge_models in one process at N = 1 — and the merged model is rendered
+    at 3840x2160 tile-parallel over the N ranks (BASELINE configs[4]), with
+    PSNR/SSIM against the GT model's render on one held-out view
+    (runtime.hpp:470-492)."""
     ctx = api.Context(dist.local)
     P = args.partitions
+    if P % dist.world != 0:
+        raise SystemExit(f"--partitions {P} must be a multiple of the GPU count {dist.world}")
     n_total = args.n_total or scenes.SIZES[args.workload]
     t0 = time.time()
     pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
     nn = api.median_nn_spacing(pts, ctx=ctx)
     parts = api.partition_cloud(pts, P, 3.0 * nn, ctx=ctx)
     rig = scenes.rig_for_cloud(pts, args.az, args.el, args.res)
-    train_idx, _ = split_rig(len(rig), 0.1, 1)
+    train_idx, test_idx = split_rig(len(rig), 0.1, 1)
     cams = [rig[i] for i in train_idx]
     rcfg = RenderConfig()
     mine = [k for k in range(P) if k % dist.world == dist.rank]
+    npix = args.res * args.res
+    resident_bytes = len(mine) * len(cams) * npix * 13
+    stream = args.stream_views or resident_bytes > 60e9
+    horizon = max(args.warmup, args.steps)
     work = []
     for k in mine:
         part = parts[k]
         idx = np.concatenate([part.owned_indices, part.ghost_indices]).astype(np.int64)
         ppts, pcols = np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx])
         gt = api.ground_truth_model(ppts, pcols, nn, 0.97, ctx=ctx)
-        views = api.DeviceViews.synthesize(ctx, gt, rcfg, cams, ppts, True, 2.0, 2.0)
+        if stream:
+            need = sorted(set(api.view_order(1 + k, len(cams), horizon).tolist()))
+            gts, masks = [None] * len(cams), [None] * len(cams)
+            for c0 in range(0, len(need), 8):  # render a few at a time, keep them in pinned memory
+                chunk = need[c0:c0 + 8]
+                sub = api.DeviceViews.synthesize(ctx, gt, rcfg, [cams[i] for i in chunk], ppts,
+                                                 True, 2.0, 2.0)
+                for j, vi in enumerate(chunk):
+                    gts[vi], masks[vi] = sub.download_planar(j, pin=True)
+                del sub
+            views = api.HostViews(ctx, cams, gts, masks)
+        else:
+            views = api.DeviceViews.synthesize(ctx, gt, rcfg, cams, ppts, True, 2.0, 2.0)
         del gt
         seeds = api.seed_gaussians(ppts, pcols, 3, ctx=ctx)
-        work.append((k, seeds, seeds.download(), views))
+        host = seeds.download()
+        host.origin_partition = k
+        seeds.upload(host)
+        work.append((k, seeds, host, views))
     log(f"[rank {dist.rank}] partitions {mine} of {P}: cloud {n_total:,} pts, sizes "
-        f"{[len(w[2]) for w in work]}, {len(cams)} views at {args.res}^2, setup {time.time() - t0:.1f}s")
+        f"{[len(w[2]) for w in work]}, {len(cams)} views at {args.res}^2 "
+        f"({'streamed from pinned host memory' if stream else 'resident'}), "
+        f"setup {time.time() - t0:.1f}s")
     for k, dm, host, views in work:  # warm-up
         if args.warmup > 0:
             api.train_device(dm, views, TrainConfig(iterations=args.warmup, seed=1 + k))
@@ -358,6 +429,9 @@ def run_partitioned(args, dist: Dist):
     n_local = float(sum(len(w[2]) for w in work))
     total_iters = P * args.steps
     gv = dist.sum(n_local * args.steps) / t_max
+    glob = None
+    if not args.no_global:
+        glob = partitioned_global(args, dist, ctx, work, parts, mine, pts, cols, nn, rig, test_idx)
     return {
         "metric": METRIC,
         "value": round(total_iters / t_max, 3),
@@ -372,15 +446,69 @@ def run_partitioned(args, dist: Dist):
         "dtype": DTYPE,
         "data": "synthetic",
         "config": {"workload": f"{args.workload}-shaped isosurface, {n_total:,} Gaussians in {P} slab "
-                               f"partitions (+ghosts), partition k on GPU k mod {dist.world}, "
+                               f"partitions (+ghosts), partition k on GPU k mod N, "
                                f"{args.az}x{args.el} rig at {args.res}^2",
                    "partitions": P, "gaussians": n_total, "resolution": args.res,
-                   "views": len(cams), "l2": "working set > L2"},
+                   "views": len(cams), "views_streamed": bool(stream),
+                   "l2": "working set > L2"},
+        "host": host_info(),
         "gaussian_views_per_sec": round(gv, 1),
+        "partition_sizes": [len(w[2]) for w in work],
         "e2e": None,
         "gpu_launches": int(dist.sum(float(launches))),
         "clocks": clk,
+        "global": glob,
     }
+
+
+def partitioned_global(args, dist: Dist, ctx, work, parts, mine, pts, cols, nn, rig, test_idx,
+                       reps: int = 3):
+    """Merge of the trained partitions and the tile-parallel 4K render of the
+    merged model (BASELINE configs[4]), plus its PSNR/SSIM on a test view."""
+    from paper_2509_12138_b200.types import Camera
+    comm = None
+    locs = [w[1] for w in work]
+    if dist.world > 1:
+        import torch.distributed as tdist
+        uid = [api.Comm.unique_id() if dist.rank == 0 else None]
+        tdist.broadcast_object_list(uid, src=0)
+        comm = api.Comm(ctx, uid[0], dist.world, dist.rank)
+        api.merge_allgather_multi(comm, locs, [parts[k] for k in mine])  # allocation pass
+        dist.barrier()
+        merged, n_merged, wire_ms = api.merge_allgather_multi(comm, locs, [parts[k] for k in mine])
+        merge_ms = dist.max(wire_ms)
+    else:
+        api.merge_models(locs, [parts[k] for k in mine], ctx=ctx)  # allocation pass
+        ctx.synchronize()
+        t0 = time.perf_counter()
+        merged = api.merge_models(locs, [parts[k] for k in mine], ctx=ctx)
+        merge_ms = (time.perf_counter() - t0) * 1e3
+        n_merged = merged.info()[0]
+    c0 = rig[0]
+    center = (pts.min(0) + pts.max(0)) * 0.5
+    cam = Camera(c0.position, tuple(float(v) for v in center), (0.0, 1.0, 0.0), 0.9, 3840, 2160,
+                 c0.near, c0.far)
+    api.render_distributed(comm, merged, cam, RenderConfig(), want_image=False)  # warm-up
+    ms = 0.0
+    for _ in range(reps):
+        dist.barrier()
+        _, t = api.render_distributed(comm, merged, cam, RenderConfig(), want_image=False)
+        ms += dist.max(t)
+    out = {"merged_gaussians": int(n_merged), "merge_ms": round(merge_ms, 3),
+           "render_4k_ms": round(ms / reps, 3),
+           "render_4k_mpix_per_sec": round(reps * 3840 * 2160 / (ms * 1e-3) / 1e6, 1),
+           "render_ranks": dist.world}
+    if dist.world > 1:
+        wire = 56.0 * int(n_merged) * (dist.world - 1) / dist.world  # bytes into each GPU
+        out["merge_allgather_GBps_per_gpu"] = round(wire / (merge_ms * 1e-3) / 1e9, 1)
+        comm.close()
+    if dist.rank == 0:  # held-out view: render(merged) vs render(GT model), runtime.hpp:483-492
+        gtm = api.ground_truth_model(pts, cols, nn, 0.97, ctx=ctx)
+        ps, ss = api.eval_view(merged, gtm, rig[test_idx[0]], RenderConfig(), ctx=ctx)
+        out["eval_test_view"] = {"view": int(test_idx[0]), "psnr": round(ps, 3), "ssim": round(ss, 5),
+                                 "note": f"after {args.steps + args.warmup} steps per partition"}
+        del gtm
+    return out
 
 
 def run_ours(args, dist: Dist):
@@ -478,7 +606,7 @@ def run_ours(args, dist: Dist):
     del res
 
     peak, peak_kind = load_peak()
-    roof = roofline(stage_ms, n, nv_vis, npix, n_dup, peak, peak_kind)
+    roof = roofline(stage_ms, n, nv_vis, npix, n_dup, peak, peak_kind, clk.get("sm_mhz"), work)
 
     cpu, parity = None, None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
@@ -736,6 +864,8 @@ def main():
     ap.add_argument("--partitions", type=int, default=0,
                     help="P > GPUs: fixed cloud in P partitions, k on GPU k mod N (configs 3/4)")
     ap.add_argument("--n-total", type=int, default=None, help="cloud size for --partitions")
+    ap.add_argument("--stream-views", action="store_true",
+                    help="--partitions: scheduled views in pinned host memory, streamed per step")
     args = ap.parse_args()
     if args.n_per_gpu is None:
         args.n_per_gpu = scenes.SIZES[args.workload]

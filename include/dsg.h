@@ -213,6 +213,10 @@ int dsg_views_destroy(dsg_views views);
 /* The view index used at each of `iterations` steps for a seed
  * (trainer.hpp:157-163, 174). */
 int dsg_view_order(uint64_t seed, int32_t n_views, int64_t iterations, int32_t* out);
+/* Copy device view v back in the device layout: gt planar [3][h*w] float,
+ * mask [h*w] bytes (either may be NULL) — the input of dsg_views_create_host. */
+int dsg_views_download_planar(dsg_ctx ctx, dsg_views views, int32_t v, float* gt_planar,
+                              uint8_t* mask);
 /* Copy view v back (gt [h][w][3], mask [h][w]; either may be NULL). */
 int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t v, double* ground_truth,
                        double* mask);

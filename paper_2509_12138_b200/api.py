@@ -259,6 +259,17 @@ class DeviceViews:
                                           C.c_double(dilation_px), C.byref(h)))
         return cls(ctx, h, list(cams), cams[0].width if n else 0, cams[0].height if n else 0)
 
+    def download_planar(self, i: int, pin: bool = False):
+        """View i in the device layout: ((3, h, w) float32, (h, w) uint8)."""
+        gt = np.empty((3, self.height, self.width), np.float32)
+        m = np.empty((self.height, self.width), np.uint8)
+        if pin:
+            gt, m = pinned(gt), pinned(m)
+        _check(lib().dsg_views_download_planar(self.ctx.h, self.h, C.c_int32(i),
+                                               gt.ctypes.data_as(C.c_void_p),
+                                               m.ctypes.data_as(C.c_void_p)))
+        return gt, m
+
     def download(self, i: int) -> TrainView:
         gt = np.zeros((self.height, self.width, 3))
         m = np.zeros((self.height, self.width))

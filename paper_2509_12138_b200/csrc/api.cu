@@ -1092,6 +1092,23 @@ int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t i, double* ground_t
   });
 }
 
+int dsg_views_download_planar(dsg_ctx ctx, dsg_views views, int32_t i, float* gt_planar,
+                              uint8_t* mask) {
+  return guarded([&] {
+    if (views->host) fail(kInvalidArgument, "host views are already in host memory");
+    if (i < 0 || i >= views->n) fail(kInvalidArgument, "view index out of range");
+    DeviceGuard g(ctx->device);
+    const int64_t npix = (int64_t)views->width * views->height;
+    if (gt_planar)
+      DSG_CUDA_CHECK(cudaMemcpyAsync(gt_planar, views->gt.get() + 3 * npix * i,
+                                     sizeof(float) * 3 * npix, cudaMemcpyDeviceToHost, ctx->stream));
+    if (mask)
+      DSG_CUDA_CHECK(cudaMemcpyAsync(mask, views->mask.get() + npix * i, npix,
+                                     cudaMemcpyDeviceToHost, ctx->stream));
+    DSG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int dsg_view_order(uint64_t seed, int32_t n_views, int64_t iterations, int32_t* out) {
   return guarded([&] {  // trainer.hpp:157-163, 174
     if (n_views <= 0) fail(kNoViews, "training requires at least one view");

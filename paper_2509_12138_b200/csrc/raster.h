@@ -78,6 +78,9 @@ struct Frame {
   DevBuf<uint32_t> counters;
   DevBuf<uint32_t> amb, tile_unit;  // termination fix-up: flagged pixels, tile -> first unit
   DevBuf<unsigned long long> work;  // frame_work_dev scratch
+  DevBuf<uint32_t> term_base, term_ntask;  // termination fix-up tasks (blend.cu)
+  DevBuf<uint2> term_task;
+  DevBuf<uint8_t> term_rec;
   DevBuf<uint32_t> row_hist;        // splats per tile row (render band balancing)
   // per pixel (planar fp32)
   DevBuf<float> rgb, T, dL, Tband;

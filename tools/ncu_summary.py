@@ -25,10 +25,14 @@ METRICS = [
     ("launch__registers_per_thread", "regs"),
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("smsp__inst_executed.sum", "warp inst"),
+    ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
+    ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
+    ("smsp__cycles_elapsed.avg.per_second", "SM clock"),
 ]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
          "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
-         "msecond": 1e-3, "second": 1.0}
+         "msecond": 1e-3, "second": 1.0, "cycle/nsecond": 1e9, "cycle/usecond": 1e6,
+         "cycle/msecond": 1e3, "cycle/second": 1.0, "Ghz": 1e9, "Mhz": 1e6, "hz": 1.0}
 
 
 def short(name: str) -> str:
@@ -57,12 +61,20 @@ def summarise(rows, seen, table, traffic, tag):
             continue
         vals = {}
         for m, _ in METRICS:
+            if m not in hdr:
+                vals[m] = float("nan")
+                continue
             i = hdr.index(m)
             v = float(r[i].replace(",", "")) if r[i] not in ("", "n/a") else float("nan")
             vals[m] = v * SCALE.get(units[i], 1.0) if units[i] in SCALE else v
         table.append((k, vals))
         traffic[k] = {"dram_bytes_per_launch": vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"],
                       "issue_active_pct": vals["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+                      "warp_inst_per_launch": vals["smsp__inst_executed.sum"],
+                      "fma_pipe_pct": vals["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"],
+                      "xu_pipe_pct": vals["sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"],
+                      "ncu_time_s": vals["gpu__time_duration.sum"],
+                      "ncu_sm_hz": vals["smsp__cycles_elapsed.avg.per_second"],
                       "source": f"profiles/{tag}_ncu_step.md"}
 
 
@@ -83,6 +95,8 @@ def write(tag, command, table, traffic):
                 cells.append(f"{x / 1e6:.1f} MB")
             elif m == "smsp__inst_executed.sum":
                 cells.append(f"{x / 1e6:.1f} M")
+            elif m == "smsp__cycles_elapsed.avg.per_second":
+                cells.append(f"{x / 1e6:.0f} MHz")
             else:
                 cells.append(f"{x:.1f}")
         lines.append(f"| {k} | " + " | ".join(cells) + " |")
