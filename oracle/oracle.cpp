@@ -6,8 +6,9 @@
 // the reference file:line it restates and keeps the reference's
 // floating-point evaluation order, so on the same inputs it reproduces the
 // reference bit-for-bit; tests/test_oracle_pin.py checks that against
-// oracle/_ref (the reference headers compiled unchanged) and against the
-// committed golden fixtures in tests/golden/.
+// oracle/_ref (the reference headers compiled unchanged) and
+// tests/test_golden.py against the reference-generated fixtures in
+// tests/golden/golden.npz (tests/golden/make_golden.py).
 //
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
 // load this library. The product (paper_2509_12138_b200/libdsg.so) never
