@@ -288,9 +288,11 @@ int64_t dsg_launch_count(void);
 /* Visible splats and tile duplicates of the last view binned on ctx. */
 int dsg_frame_stats(dsg_ctx ctx, int64_t* n_visible, int64_t* n_dup);
 /* Work of the last forward on ctx: composited (pixel, splat) pairs (the sum
- * of n_contrib, the blend kernels' work count C) and the pixels
- * whose termination was re-decided in fp64. */
-int dsg_frame_work(dsg_ctx ctx, int64_t* composited, int64_t* term_fixups);
+ * of n_contrib, the blend kernels' work count C), the pixels
+ * whose termination was re-decided in fp64, and how many of those the fp32
+ * walk had decided differently. Any pointer may be NULL. */
+int dsg_frame_work(dsg_ctx ctx, int64_t* composited, int64_t* term_fixups,
+                   int64_t* term_changed);
 /* Forward-render n cameras `repeats` times back to back on the device;
  * *ms = CUDA-event time (render Mpix/s measurement). */
 int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32_t n,

@@ -606,9 +606,9 @@ def frame_stats(ctx: Context):
 
 def frame_work(ctx: Context):
     """(composited pairs C, termination fix-ups) of the last forward on ctx."""
-    c, f = C.c_int64(), C.c_int64()
-    _check(lib().dsg_frame_work(ctx.h, C.byref(c), C.byref(f)))
-    return {"composited": c.value, "term_fixups": f.value}
+    c, f, ch = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib().dsg_frame_work(ctx.h, C.byref(c), C.byref(f), C.byref(ch)))
+    return {"composited": c.value, "term_fixups": f.value, "term_changed": ch.value}
 
 
 def render_timed(dmodel: DeviceModel, cams, cfg: RenderConfig, repeats: int = 1) -> float:

@@ -1575,13 +1575,15 @@ int dsg_nvtx_pop(void) {
   return 0;
 }
 
-int dsg_frame_work(dsg_ctx ctx, int64_t* composited, int64_t* term_fixups) {
+int dsg_frame_work(dsg_ctx ctx, int64_t* composited, int64_t* term_fixups,
+                   int64_t* term_changed) {
   return guarded([&] {
     DeviceGuard g(ctx->device);
-    int64_t c = 0, f = 0;
-    frame_work_dev(ctx->frame, ctx->stream, &c, &f);
+    int64_t c = 0, f = 0, ch = 0;
+    frame_work_dev(ctx->frame, ctx->stream, &c, &f, &ch);
     if (composited) *composited = c;
     if (term_fixups) *term_fixups = f;
+    if (term_changed) *term_changed = ch;
   });
 }
 

@@ -253,7 +253,8 @@ void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, 
                      double lambda, cudaStream_t st, double* out = nullptr);
 
 // sum of n_contrib of the last forward and the termination fix-ups (host values)
-void frame_work_dev(Frame& f, cudaStream_t st, int64_t* composited, int64_t* fixups);
+void frame_work_dev(Frame& f, cudaStream_t st, int64_t* composited, int64_t* fixups,
+                    int64_t* changed = nullptr);
 // psnr / ssim (metrics.hpp:20-38) of planar fp32 RGB images; out = {psnr, ssim} (device)
 void image_metrics_dev(Frame& f, const float* x, const float* y, int width, int height,
                        cudaStream_t st, double* out);
