@@ -156,7 +156,7 @@ def build_partition_inputs(args, dist: Dist, ctx):
     if args.workload == "kingsnake":
         pts, cols, _ = scenes.kingsnake(n_total, seed=1, turns=6.0 * dist.world)
     else:
-        pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
+        pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1, ctx=ctx)
     nn = api.median_nn_spacing(pts, ctx=ctx)          # resolve_auto_values (runtime.hpp:73-77)
     margin = 3.0 * nn
     parts = api.partition_cloud(pts, dist.world, margin, ctx=ctx)  # partition.hpp:42-104, on device
@@ -366,7 +366,8 @@ def run_partitioned(args, dist: Dist):
         raise SystemExit(f"--partitions {P} must be a multiple of the GPU count {dist.world}")
     n_total = args.n_total or scenes.SIZES[args.workload]
     t0 = time.time()
-    pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1)
+    pts, cols, _ = scenes.make_cloud(args.workload, n_total, seed=1, ctx=ctx)
+    log(f"[rank {dist.rank}] cloud {n_total:,} pts generated in {time.time() - t0:.1f}s")
     nn = api.median_nn_spacing(pts, ctx=ctx)
     parts = api.partition_cloud(pts, P, 3.0 * nn, ctx=ctx)
     rig = scenes.rig_for_cloud(pts, args.az, args.el, args.res)

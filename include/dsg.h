@@ -124,6 +124,16 @@ int dsg_cloud_save_ply(const char* path, const double* positions, const double* 
 int dsg_cloud_load_ply(const char* path, double* positions, double* normals, double* colors,
                        int64_t capacity, int64_t* n);
 
+/* ---- synthetic inputs ----------------------------------------- */
+/* RT/RM-shaped isosurface cloud y = h(x, z) of n points generated on the
+ * device (scene.cu): jittered lattice with hash_combine jitter (rng.hpp:17-20),
+ * modes [nmodes][5] = (kx, kz, phase_x, phase_z, amplitude), bubble/spike
+ * nonlinearity `spikes`, normal_matte colours (marching_cubes.hpp:21-29);
+ * outputs [n][3] fp32-exact doubles (any may be NULL). scenes.py restates it. */
+int dsg_heightfield_cloud(dsg_ctx ctx, int64_t n, uint64_t seed, double span, double amp,
+                          double spikes, int32_t nmodes, const double* modes, double* positions,
+                          double* colors, double* normals);
+
 /* ---- evaluation (metrics.hpp:20-38, runtime.hpp:483-492) ---------------------- */
 /* psnr (capped at 99) and mean windowed SSIM of two HWC double RGB images. */
 int dsg_image_metrics(dsg_ctx ctx, const double* a, const double* b, int32_t width,

@@ -789,3 +789,17 @@ def eval_view(model, truth, cam: Camera, cfg: RenderConfig, ctx: Context = None)
     _check(lib().dsg_eval_view(ctx.h, dm.h, dt.h, C.byref(cam_struct(cam)),
                                C.byref(cfg_struct(cfg)), C.byref(ps), C.byref(ss)))
     return ps.value, ss.value
+
+
+def heightfield_cloud(kind: str, n: int, seed: int = 1, ctx: Context = None):
+    """RT/RM-shaped cloud (positions, colors, normals) generated on the device
+    (dsg_heightfield_cloud); scenes._heightfield is its numpy restatement."""
+    from .scenes import HEIGHTFIELDS, heightfield_modes
+    ctx = ctx or default_context()
+    hp = HEIGHTFIELDS[kind]
+    modes = np.ascontiguousarray(heightfield_modes(seed, hp["modes"], hp["amp"], hp["span"]))
+    out = [np.empty((n, 3)) for _ in range(3)]
+    _check(lib().dsg_heightfield_cloud(ctx.h, C.c_int64(n), C.c_uint64(seed), C.c_double(hp["span"]),
+                                       C.c_double(hp["amp"]), C.c_double(hp["spikes"]),
+                                       C.c_int32(hp["modes"]), _p(modes), *[_p(a) for a in out]))
+    return out[0], out[1], out[2]

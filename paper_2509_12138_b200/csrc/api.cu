@@ -1617,6 +1617,36 @@ int dsg_render_timed(dsg_ctx ctx, dsg_model model, const dsg_camera* cams, int32
   });
 }
 
+int dsg_heightfield_cloud(dsg_ctx ctx, int64_t n, uint64_t seed, double span, double amp,
+                          double spikes, int32_t nmodes, const double* modes, double* positions,
+                          double* colors, double* normals) {
+  return guarded([&] {
+    if (n <= 0) fail(kEmptyCloud, "empty cloud");
+    if (nmodes < 0 || (nmodes > 0 && !modes)) fail(kInvalidArgument, "bad mode table");
+    DeviceGuard g(ctx->device);
+    cudaStream_t st = ctx->stream;
+    // generated in slices so the device scratch stays bounded at any size
+    const int64_t slice = int64_t(1) << 24;
+    DevBuf<double> buf;
+    buf.ensure(9 * (size_t)std::min(n, slice));
+    for (int64_t s0 = 0; s0 < n; s0 += slice) {
+      const int64_t m = std::min(slice, n - s0);
+      heightfield_slice_dev(n, s0, m, seed, span, amp, spikes, nmodes, modes, buf.get(),
+                            buf.get() + 3 * m, buf.get() + 6 * m, st);
+      if (positions)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(positions + 3 * s0, buf.get(), sizeof(double) * 3 * m,
+                                       cudaMemcpyDeviceToHost, st));
+      if (colors)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(colors + 3 * s0, buf.get() + 3 * m, sizeof(double) * 3 * m,
+                                       cudaMemcpyDeviceToHost, st));
+      if (normals)
+        DSG_CUDA_CHECK(cudaMemcpyAsync(normals + 3 * s0, buf.get() + 6 * m, sizeof(double) * 3 * m,
+                                       cudaMemcpyDeviceToHost, st));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
+  });
+}
+
 int dsg_image_metrics(dsg_ctx ctx, const double* a, const double* b, int32_t width,
                       int32_t height, double* psnr, double* ssim) {
   return guarded([&] {  // psnr / ssim (metrics.hpp:20-38) of two HWC double RGB images

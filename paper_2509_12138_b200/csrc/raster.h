@@ -259,6 +259,11 @@ void frame_work_dev(Frame& f, cudaStream_t st, int64_t* composited, int64_t* fix
 void image_metrics_dev(Frame& f, const float* x, const float* y, int width, int height,
                        cudaStream_t st, double* out);
 
+// RT/RM-shaped heightfield clouds on the device (scene.cu); outputs device [n][3]
+void heightfield_slice_dev(int64_t n, int64_t s0, int64_t m, uint64_t seed, double span,
+                           double amp, double spikes, int nmodes, const double* modes_host,
+                           double* pos, double* col, double* nrm, cudaStream_t st);
+
 // float64 PLY (ply_io.hpp:89-221, io.cu)
 struct PlyInfo {
   int64_t vertex_count = 0;

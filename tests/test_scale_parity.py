@@ -110,8 +110,8 @@ def test_config2_knn_seeds_at_scale(ctx):
 
 
 @pytest.fixture(scope="module")
-def rt_cloud():
-    return scenes.rt(scenes.SIZES["rt"], seed=1)
+def rt_cloud(ctx):
+    return scenes.make_cloud("rt", scenes.SIZES["rt"], seed=1, ctx=ctx)  # device generator
 
 
 def test_config3_rt_partition_bit_exact(ctx, ref, rt_cloud):
