@@ -580,11 +580,30 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   DSG_CUDA_CHECK(cudaMemcpyAsync(&nd, f.offs.get() + nv, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   DSG_CUDA_CHECK(cudaMemcpyAsync(&n_long, long_runs, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (n_long > 0) {
+  if (n_long > kLongCap) {
+    // very rare: more long near-coincident runs than the per-run path takes.
+    // Sort the whole visible set by (fp64 depth bits, index) instead — the
+    // reference comparator (render.hpp:98-101): depths are > near > 0, so
+    // their bit patterns order as the values, and a stable sort of the
+    // index-ordered compaction breaks ties by index.
+    unsigned long long* rk = f.run_keys.ensure(2 * (size_t)nv);
+    uint32_t* rv = f.run_vals.ensure(2 * (size_t)nv);
+    k_vis_compact<<<blocks(n, 256), 256, 0, st>>>(f.tcount.get(), f.depth.get(), f.drange.get(),
+                                                  f.vslot.get(), n, cnt, rv);
+    k_run_keys<<<blocks(nv, 256), 256, 0, st>>>(rv, 0, (uint32_t)nv, f.depth.get(), rk, rv + nv);
+    count_launch(2);
+    const bool in_alt = radix_sort_pairs<uint64_t>(
+        reinterpret_cast<uint64_t*>(rk), rv + nv, reinterpret_cast<uint64_t*>(rk) + nv, rv, nv, 0,
+        64, f.sort, st);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(sidx, in_alt ? rv : rv + nv, sizeof(uint32_t) * nv,
+                                   cudaMemcpyDeviceToDevice, st));
+    k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+    count_launch();
+    exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
+  } else if (n_long > 0) {
     // rare: long runs of near-coincident depths with out-of-order pairs.
     // Radix-sort each by its fp64 depth bits, then redo the slots (the
     // duplicate total is order-independent).
-    if (n_long > kLongCap) fail(kInvalidArgument, "too many long equal-depth runs");
     std::vector<uint32_t> runs(2 * n_long);
     DSG_CUDA_CHECK(cudaMemcpy(runs.data(), long_runs + 1, sizeof(uint32_t) * 2 * n_long,
                               cudaMemcpyDeviceToHost));

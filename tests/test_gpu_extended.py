@@ -312,3 +312,40 @@ def test_device_heightfield_matches_numpy(ctx, kind):
     # any slice of the cloud depends only on (seed, index): a prefix of a
     # larger cloud with the same lattice side is identical
     np.testing.assert_array_equal(scenes.make_cloud(kind, n, seed=3, ctx=ctx)[0], a[0])
+
+
+def _coincident_clusters(nclusters=1100, per=80):
+    """nclusters clusters of `per` splats whose camera depths differ by less
+    than the depth-key quantum, in reverse index order: every cluster is a
+    long run of equal keys that needs the exact (fp64 depth, index) order."""
+    rng = np.random.default_rng(5)
+    P = np.zeros((nclusters * per, 14))
+    side = int(np.ceil(np.sqrt(nclusters)))
+    k = 0
+    for c in range(nclusters):
+        cx = ((c % side) / side - 0.5) * 1.6
+        cy = ((c // side) / side - 0.5) * 1.6
+        cz = rng.uniform(0.0, 8.0)
+        for j in range(per):
+            P[k, 0:3] = [cx - j * 2.0 ** -16, cy, cz]
+            k += 1
+    P[:, 3:6] = np.log(0.002)
+    P[:, 6] = 1.0
+    P[:, 10] = 2.0
+    P[:, 11:14] = 0.5
+    return fp32_exact(SplatModel(P))
+
+
+def test_more_long_runs_than_the_per_run_path(orc, ctx):
+    """More than kLongCap (1024) long near-coincident runs: the whole visible
+    set is sorted by (fp64 depth bits, index) instead of failing (round 1
+    raised InvalidArgument here). 1053 such runs in this scene (checked on
+    the CPU by replaying the device's key quantisation)."""
+    from paper_2509_12138_b200.types import Camera
+    m = _coincident_clusters()
+    cam = Camera((0.0, 0.0, -3.0), (3e-7, 0.0, 0.0), (0.0, 1.0, 0.0), 1.2, 128, 128, 0.1, 50.0)
+    a = api.render(m, cam, RenderConfig(), ctx=ctx)
+    b = orc.render(m, cam, RenderConfig())
+    np.testing.assert_array_equal(a.splat_order, b.splat_order)
+    assert np.max(np.abs(a.color - b.color)) <= 1e-3
+    np.testing.assert_array_equal(a.per_pixel_contributor_count, b.per_pixel_contributor_count)
