@@ -596,6 +596,7 @@ def run_ours(args, dist: Dist):
     res = api.train_partition_full(host_model, tviews, tc, ctx=ctx, loss_trace=True)
     e_wall = time.perf_counter() - e0
     gc.enable()
+    log(f"[e2e] wall {e_wall:.4f}s phases {getattr(ctx, 'last_phases', None)}")
     e_dev_ms, _ = ctx.last_timing()  # the same loop's device span (events)
     e_parts = {"train_partition_full_s": round(e_wall, 4), "train_device_s": round(e_dev_ms * 1e-3, 4),
                **{k: round(v, 4) for k, v in getattr(ctx, "last_phases", {}).items()},

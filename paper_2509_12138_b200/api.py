@@ -446,13 +446,14 @@ def train_partition_full(model: SplatModel, views, cfg: TrainConfig, shards: int
                          checkpoint=None, progress=None, ctx: Context = None,
                          loss_trace: bool = False) -> TrainResult:
     """train_partition_full (trainer.hpp:140-211): host in, host out."""
+    import time
+    t_in = time.perf_counter()
     ctx = ctx or default_context()
     cfg.validate()
     if len(views) == 0:
         raise DsplatError(ErrorCode.NoViews, "training requires at least one view")
     if shards < 1:
         raise DsplatError(ErrorCode.InvalidArgument, "shards must be >= 1")
-    import time
     t0 = time.perf_counter()
     dm = ctx.scratch_model(model)
     t1 = time.perf_counter()
@@ -461,13 +462,18 @@ def train_partition_full(model: SplatModel, views, cfg: TrainConfig, shards: int
     fl, trace = train_device(dm, dv, cfg, shards, progress, loss_trace, checkpoint=checkpoint,
                              origin=model.origin_partition)
     t3 = time.perf_counter()
+    del dv  # frees the two device view slots
+    t3b = time.perf_counter()
     out = dm.download()
     out.origin_partition = model.origin_partition
     res = TrainResult(out, fl, len(model), len(out))
     if trace is not None:
         res.loss_trace = trace
-    ctx.last_phases = {"upload_s": t1 - t0, "views_s": t2 - t1, "train_s": t3 - t2,
-                       "download_s": time.perf_counter() - t3}
+    t4 = time.perf_counter()
+    res.model.params  # noqa: B018
+    ctx.last_phases = {"enter_s": t0 - t_in, "upload_s": t1 - t0, "views_s": t2 - t1,
+                       "train_s": t3 - t2, "views_free_s": t3b - t3, "download_s": t4 - t3b,
+                       "result_s": time.perf_counter() - t4}
     return res
 
 

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -486,7 +487,12 @@ class HostPool {
 
  private:
   HostPool() : pid_(getpid()) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    // ranks of one node share its cores (torchrun sets LOCAL_WORLD_SIZE)
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) {
+      const int k = std::atoi(lw);
+      if (k > 1) hw = std::max(1u, hw / (unsigned)k);
+    }
     for (unsigned k = 1; k < std::min(hw, 16u); ++k)
       workers_.emplace_back([this] { loop(); });
   }

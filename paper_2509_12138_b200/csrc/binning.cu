@@ -7,11 +7,14 @@
 // key lists match the x86-64 reference bit-for-bit; the blend payload is
 // stored as fp32 (mean2d as a hi/lo pair so pixel offsets stay exact).
 //
-// Ordering: visible splats are sorted by fp32 depth bits (monotone in the
-// fp64 depth), runs of equal fp32 keys are re-ordered by (fp64 depth, index)
-// — the reference comparator (render.hpp:98-101) — and the duplicates are
-// then stably sorted by tile id, so every tile list is in reference
-// compositing order.
+// Ordering: visible splats are sorted by a 32-bit key, the fp64 depth
+// quantised over the visible depth range (monotone in the fp64 depth); the
+// compaction is index-ordered and the sort stable, so only runs of equal keys
+// with out-of-order neighbours need work: short ones are insertion-sorted,
+// long ones radix-sorted by fp64 depth bits, and past kLongCap long runs the
+// whole visible set is sorted by (fp64 depth bits, index) — the reference
+// comparator (render.hpp:98-101). The duplicates are then stably sorted by
+// tile id, so every tile list is in reference compositing order.
 #include <atomic>
 #include <cstdlib>
 

@@ -129,3 +129,25 @@ def test_merge_allgather_and_band_render(tmp_path, world):
     os.makedirs(os.path.dirname(log), exist_ok=True)
     with open(log, "w") as f:
         f.write(r.stdout)
+
+
+def test_loss_on_two_devices_in_one_process():
+    """The SSIM window is a kernel parameter: a second context on another
+    device computes the same loss (round-1 advisor: a once-per-process
+    constant upload left device 1 with zero weights)."""
+    if _ngpus() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from paper_2509_12138_b200 import api
+    from paper_2509_12138_b200.types import TrainView
+    from util import disc_mask
+    from util import test_camera as make_camera
+    rng = np.random.default_rng(3)
+    a = rng.random((40, 36, 3)).astype(np.float32).astype(np.float64)
+    b = np.clip(a + rng.normal(scale=0.05, size=a.shape), 0, 1)
+    view = TrainView(make_camera(36), b, disc_mask(36, 40, 17.0, 20.0, 14.0))
+    view.cam.height = 40
+    l0 = api.masked_loss(a, view, 0.2, ctx=api.Context(0))
+    l1 = api.masked_loss(a, view, 0.2, ctx=api.Context(1))
+    assert l0.loss == l1.loss and l0.loss > 0.0
+    np.testing.assert_array_equal(l0.dL_dpixels, l1.dL_dpixels)
