@@ -92,6 +92,10 @@ struct dsg_ctx_s {
   // pinned per-step view slots of reference-layout host views (planar fp32 + u8)
   char* vpin[2] = {nullptr, nullptr};
   size_t vpin_bytes = 0;
+  // device slots of streamed (host) views, owned by the context so creating
+  // and destroying host view sets never allocates device memory
+  DevBuf<float> vslot_gt;
+  DevBuf<uint8_t> vslot_mask;
   cudaEvent_t pin_ev[2] = {nullptr, nullptr};
   double last_total_ms = 0.0;
   int64_t last_iters = 0;
@@ -1076,6 +1080,7 @@ int dsg_views_destroy(dsg_views views) {
 int dsg_views_download(dsg_ctx ctx, dsg_views views, int32_t i, double* ground_truth,
                        double* mask) {
   return guarded([&] {
+    if (views->host) fail(kInvalidArgument, "host views are already in host memory");
     if (i < 0 || i >= views->n) fail(kInvalidArgument, "view index out of range");
     DeviceGuard g(ctx->device);
     const int64_t npix = (int64_t)views->width * views->height;
@@ -1145,10 +1150,6 @@ int dsg_views_create_host(dsg_ctx ctx, const dsg_camera* cams, const float* cons
         v->host_gt.push_back(gt_planar ? gt_planar[i] : nullptr);
         v->host_mask.push_back(masks ? masks[i] : nullptr);
       }
-      DeviceGuard g(ctx->device);
-      const int64_t npix = (int64_t)v->width * v->height;
-      v->gt.ensure(std::max<int64_t>(1, 2 * 3 * npix));
-      v->mask.ensure(std::max<int64_t>(1, 2 * npix));
     } catch (...) {
       delete v;
       throw;
@@ -1180,10 +1181,6 @@ int dsg_views_create_host_ref(dsg_ctx ctx, const dsg_camera* cams,
         v->host_gt64.push_back(ground_truth ? ground_truth[i] : nullptr);
         v->host_mask64.push_back(masks ? masks[i] : nullptr);
       }
-      DeviceGuard g(ctx->device);
-      const int64_t npix = (int64_t)v->width * v->height;
-      v->gt.ensure(std::max<int64_t>(1, 2 * 3 * npix));
-      v->mask.ensure(std::max<int64_t>(1, 2 * npix));
     } catch (...) {
       delete v;
       throw;
@@ -1287,6 +1284,8 @@ int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
       }
       ctx->vpin_bytes = (size_t)(13 * npix);
     }
+    float* slot_gt = views->host ? ctx->vslot_gt.ensure(2 * 3 * (size_t)npix) : nullptr;
+    uint8_t* slot_mask = views->host ? ctx->vslot_mask.ensure(2 * (size_t)npix) : nullptr;
     auto copy_view = [&](int64_t step) {
       const size_t v = order[(size_t)step % order.size()];
       const int slot = (int)(step & 1);
@@ -1305,9 +1304,9 @@ int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
         src_mask = pm;
       }
       DSG_CUDA_CHECK(cudaStreamWaitEvent(cs, ctx->ev_consumed[slot], 0));
-      DSG_CUDA_CHECK(cudaMemcpyAsync(views->gt.get() + 3 * npix * slot, src_gt,
+      DSG_CUDA_CHECK(cudaMemcpyAsync(slot_gt + 3 * npix * slot, src_gt,
                                      sizeof(float) * 3 * npix, cudaMemcpyHostToDevice, cs));
-      DSG_CUDA_CHECK(cudaMemcpyAsync(views->mask.get() + npix * slot, src_mask, npix,
+      DSG_CUDA_CHECK(cudaMemcpyAsync(slot_mask + npix * slot, src_mask, npix,
                                      cudaMemcpyHostToDevice, cs));
       DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_copied[slot], cs));
     };
@@ -1321,8 +1320,10 @@ int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
       const size_t vi = order[(size_t)it % order.size()];
       const CamDev& cam = cams[vi];
       const int slot = (int)(it & 1);
-      const float* gt = views->gt.get() + 3 * npix * (views->host ? (size_t)slot : vi);
-      const uint8_t* mk = views->mask.get() + npix * (views->host ? (size_t)slot : vi);
+      const float* gt = views->host ? slot_gt + 3 * npix * (size_t)slot
+                                    : views->gt.get() + 3 * npix * vi;
+      const uint8_t* mk = views->host ? slot_mask + npix * (size_t)slot
+                                      : views->mask.get() + npix * vi;
       if (views->host) {
         DSG_CUDA_CHECK(cudaStreamWaitEvent(st, ctx->ev_copied[slot], 0));
         if (it + 1 < iters) copy_view(it + 1);
