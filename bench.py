@@ -45,6 +45,7 @@ METRIC = "training iters/sec & Gaussians·views/sec at 1/2/4/8 B200; render Mpix
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 TRAFFIC_PATH = os.path.join(ROOT, "profiles", "traffic.json")
 FALLBACK_HBM = 6650.0  # GB/s, B200_PROFILING.md fallback
+NVLINK_GBPS = 900.0    # NVLink 5 per direction per GPU (B200_PROFILING.md)
 # arithmetic type of the path: fp32 storage and blend/chain/Adam arithmetic;
 # fp64 where an integer or ordering decision is taken (projection, rects,
 # depth order, the alpha/cutoff guard band) and in the SSIM window sums
@@ -211,8 +212,12 @@ def global_phase(args, dist: Dist, ctx, inp, trained, reps: int = 3):
     mpix = reps * 3840 * 2160 / (ms * 1e-3) / 1e6
     mm = dist.max(merge_ms)
     wire = 56.0 * int(n_merged) * (dist.world - 1) / max(dist.world, 1)  # bytes into each GPU
+    gbs = wire / (mm * 1e-3) / 1e9 if dist.world > 1 else None
     return {"merged_gaussians": int(n_merged), "merge_allgather_ms": round(mm, 3),
-            "merge_allgather_GBps_per_gpu": round(wire / (mm * 1e-3) / 1e9, 1) if dist.world > 1 else None,
+            "merge_allgather_GBps_per_gpu": round(gbs, 1) if gbs else None,
+            "merge_vs_nvlink": ({"peak_GBps_per_direction": NVLINK_GBPS, "frac": round(gbs / NVLINK_GBPS, 3)}
+                                if gbs else None),
+            "merge_exchange": api.merge_exchange() if gbs else "one process",
             "render_4k_ms": round(ms / reps, 3), "render_4k_mpix_per_sec": round(mpix, 1),
             "render_ranks": dist.world}
 
@@ -501,7 +506,10 @@ def partitioned_global(args, dist: Dist, ctx, work, parts, mine, pts, cols, nn, 
            "render_ranks": dist.world}
     if dist.world > 1:
         wire = 56.0 * int(n_merged) * (dist.world - 1) / dist.world  # bytes into each GPU
-        out["merge_allgather_GBps_per_gpu"] = round(wire / (merge_ms * 1e-3) / 1e9, 1)
+        gbs = wire / (merge_ms * 1e-3) / 1e9
+        out["merge_allgather_GBps_per_gpu"] = round(gbs, 1)
+        out["merge_vs_nvlink"] = {"peak_GBps_per_direction": NVLINK_GBPS, "frac": round(gbs / NVLINK_GBPS, 3)}
+        out["merge_exchange"] = api.merge_exchange()
         comm.close()
     if dist.rank == 0:  # held-out view: render(merged) vs render(GT model), runtime.hpp:483-492
         gtm = api.ground_truth_model(pts, cols, nn, 0.97, ctx=ctx)

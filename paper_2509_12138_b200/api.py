@@ -729,6 +729,13 @@ def merge_allgather_multi(comm: Comm, locals_, partitions) -> tuple:
     return merged, n.value, ms.value
 
 
+def merge_exchange() -> str:
+    """'peer' (NVLink pulls through CUDA IPC) or 'nccl' for the last merge."""
+    L = lib()
+    L.dsg_merge_exchange.restype = C.c_char_p
+    return L.dsg_merge_exchange().decode()
+
+
 def render_distributed(comm, model: DeviceModel, cam: Camera, cfg: RenderConfig, want_image=True):
     """Tile-parallel render with the bands gathered to rank 0 (comm may be None)."""
     ctx = model.ctx

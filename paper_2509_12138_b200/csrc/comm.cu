@@ -15,6 +15,7 @@
 // NCCL is loaded with dlopen so the process shares whichever libnccl is
 // already resident (e.g. torch's) instead of mapping a second copy.
 #include <dlfcn.h>
+#include <cstdlib>
 #include <nccl.h>
 
 #include <string>
@@ -24,6 +25,8 @@
 #include "raster.h"
 
 namespace dsg {
+
+const char* g_merge_path = "none";  // last merge exchange: "peer" or "nccl"
 
 namespace {
 
@@ -35,6 +38,8 @@ struct Nccl {
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -59,6 +64,7 @@ Nccl& nccl() {
   n.CommDestroy = (decltype(n.CommDestroy))sym("ncclCommDestroy");
   n.AllGather = (decltype(n.AllGather))sym("ncclAllGather");
   n.Broadcast = (decltype(n.Broadcast))sym("ncclBroadcast");
+  n.AllReduce = (decltype(n.AllReduce))sym("ncclAllReduce");
   n.Send = (decltype(n.Send))sym("ncclSend");
   n.Recv = (decltype(n.Recv))sym("ncclRecv");
   n.GroupStart = (decltype(n.GroupStart))sym("ncclGroupStart");
@@ -133,7 +139,121 @@ __global__ void k_unpack_records(const float* __restrict__ rec, int64_t maxc, in
   if (i >= cnt[r]) return;  // padding
   P[k * pitch + off[r] + i] = rec[t];
 }
+// One partition's packed records [cnt][14], read straight from the owning
+// GPU's memory over NVLink (CUDA IPC mapping), transposed through shared
+// memory into the merged planar store at `off`: the transfer and the layout
+// change are one kernel. Coalesced 16 B loads (records start 16 B aligned:
+// partitions are padded to an even count), coalesced plane stores.
+constexpr int kPeerRecs = 256;
+__global__ void __launch_bounds__(256) k_peer_unpack(const float* __restrict__ src, int64_t cnt,
+                                                     float* __restrict__ P, int64_t pitch,
+                                                     int64_t off) {
+  __shared__ float4 sm4[kPeerRecs * kParams / 4];
+  float* sm = reinterpret_cast<float*>(sm4);
+  const int64_t b0 = (int64_t)blockIdx.x * kPeerRecs;
+  const int nrec = (int)(cnt - b0 < kPeerRecs ? cnt - b0 : (int64_t)kPeerRecs);
+  const float4* s4 = reinterpret_cast<const float4*>(src + b0 * kParams);
+  const int nf4 = (nrec * kParams + 3) / 4;  // the source is padded to whole float4s
+  for (int i = threadIdx.x; i < nf4; i += blockDim.x) sm4[i] = s4[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrec * kParams; i += blockDim.x) {
+    const int c = i / nrec, r = i - c * nrec;
+    P[c * pitch + off + b0 + r] = sm[r * kParams + c];
+  }
+}
 }  // namespace
+
+// Peer-memory variant of step 3 (default; DSG_MERGE_PATH=nccl selects the
+// all-gather): every rank packs all its partitions' survivors into one
+// buffer, publishes its CUDA IPC handle (an all-gather of 64 B handles,
+// which also orders it after every rank's packing), and then pulls each
+// partition's records from the owning GPU with k_peer_unpack — NVLink reads
+// and the planar scatter in one pass. An all-reduce of one word after the
+// pulls tells every rank its buffer is no longer read.
+static bool merge_from_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
+                             const std::vector<DevBuf<float>>& dense,
+                             const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
+                             ModelDev& merged, cudaStream_t st, float* wire_ms) {
+  const int P = nranks * nlocal;
+  // my partitions' records, each padded to an even count (16 B-aligned starts)
+  std::vector<int64_t> roff(nlocal + 1, 0);
+  for (int j = 0; j < nlocal; ++j) roff[j + 1] = roff[j] + ((cnt[j * nranks + rank] + 1) & ~int64_t(1));
+  DevBuf<float> send;
+  send.ensure((size_t)std::max<int64_t>(roff[nlocal], 2) * kParams + 4);
+  for (int j = 0; j < nlocal; ++j) {
+    const int64_t my = cnt[j * nranks + rank];
+    if (my > 0) {
+      k_pack_records<<<(unsigned)((my * kParams + 255) / 256), 256, 0, st>>>(
+          dense[j].get(), std::max<int64_t>(my, 1), my, send.get() + roff[j] * kParams);
+      count_launch();
+    }
+  }
+  // publish the buffer; the all-gather completes only after every rank packed
+  cudaIpcMemHandle_t mine;
+  if (cudaIpcGetMemHandle(&mine, send.get()) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  DevBuf<uint8_t> hbuf;
+  hbuf.ensure((size_t)64 * (nranks + 1));
+  DSG_CUDA_CHECK(cudaMemcpyAsync(hbuf.get() + 64 * nranks, &mine, 64, cudaMemcpyHostToDevice, st));
+  nc(N.AllGather(hbuf.get() + 64 * nranks, hbuf.get(), 64, ncclUint8, c, st), "allgather handles");
+  std::vector<cudaIpcMemHandle_t> hs(nranks);
+  DSG_CUDA_CHECK(cudaMemcpyAsync(hs.data(), hbuf.get(), 64 * nranks, cudaMemcpyDeviceToHost, st));
+  // every rank's record offsets (the same padding rule, from the counts)
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::vector<const float*> src(nranks, nullptr);
+  bool ok = true;
+  for (int r = 0; r < nranks; ++r) {
+    if (r == rank) {
+      src[r] = send.get();
+      continue;
+    }
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      continue;
+    }
+    src[r] = static_cast<const float*>(p);
+  }
+  // every rank must agree before anyone relies on peer reads
+  DevBuf<int> flag;
+  flag.ensure(1);
+  const int okv = ok ? 1 : 0;
+  DSG_CUDA_CHECK(cudaMemcpyAsync(flag.get(), &okv, sizeof(int), cudaMemcpyHostToDevice, st));
+  nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce ipc status");
+  int all_ok = 0;
+  DSG_CUDA_CHECK(cudaMemcpyAsync(&all_ok, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (all_ok) {
+    cudaEvent_t e0, e1;
+    DSG_CUDA_CHECK(cudaEventCreate(&e0));
+    DSG_CUDA_CHECK(cudaEventCreate(&e1));
+    DSG_CUDA_CHECK(cudaEventRecord(e0, st));
+    for (int k = 0; k < P; ++k) {  // partition order
+      const int r = k % nranks, j = k / nranks;
+      if (cnt[k] == 0) continue;
+      int64_t ro = 0;  // rank r's record offset of its j-th partition
+      for (int jj = 0; jj < j; ++jj) ro += (cnt[jj * nranks + r] + 1) & ~int64_t(1);
+      k_peer_unpack<<<(unsigned)((cnt[k] + kPeerRecs - 1) / kPeerRecs), 256, 0, st>>>(
+          src[r] + ro * kParams, cnt[k], merged.params.get(), merged.cap, off[k]);
+      count_launch();
+    }
+    DSG_CUDA_CHECK(cudaEventRecord(e1, st));
+    // nobody frees or reuses a buffer a peer may still be reading
+    nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce done");
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    float t = 0.f;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (wire_ms) *wire_ms = t;
+  }
+  for (int r = 0; r < nranks; ++r)
+    if (r != rank && src[r]) cudaIpcCloseMemHandle(const_cast<float*>(src[r]));
+  return all_ok != 0;
+}
 
 // Steps 1-3 above. `merged` receives the merged model (reserved inside).
 // Rank r holds partitions k = j * nranks + r for j < nlocal (partition k on
@@ -190,7 +310,18 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* co
   DSG_CUDA_CHECK(cudaMemcpyAsync(co.get() + P, off.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice, st));
   merged.reserve(std::max<int64_t>(total, 1));
   merged.n = total;
-  // 3. pack, all-gather, unpack, round by round
+  // 3a. peer-memory pull (default)
+  static const bool use_nccl = [] {
+    const char* e = std::getenv("DSG_MERGE_PATH");
+    return e && std::string(e) == "nccl";
+  }();
+  if (!use_nccl && nranks > 1 &&
+      merge_from_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms)) {
+    g_merge_path = "peer";
+    return total;
+  }
+  g_merge_path = "nccl";
+  // 3b. pack, all-gather, unpack, round by round
   int64_t maxc_all = 1;
   for (int k = 0; k < P; ++k) maxc_all = std::max(maxc_all, cnt[k]);
   DevBuf<float> send, recv;

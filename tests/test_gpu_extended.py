@@ -349,3 +349,33 @@ def test_more_long_runs_than_the_per_run_path(orc, ctx):
     np.testing.assert_array_equal(a.splat_order, b.splat_order)
     assert np.max(np.abs(a.color - b.color)) <= 1e-3
     np.testing.assert_array_equal(a.per_pixel_contributor_count, b.per_pixel_contributor_count)
+
+
+def test_view_sources_train_identically(orc, ctx):
+    """The three view sources of dsg_train — device-resident views, planar
+    views streamed from pinned host memory (dsg_views_create_host, used by
+    the partitioned bench) and reference-layout TrainViews converted per
+    step (dsg_views_create_host_ref, used by train_partition_full) — give
+    bit-identical trajectories."""
+    pts, cols, _ = scenes.sphere(6000)
+    cams = scenes.rig_for_cloud(pts, 4, 2, 96)[:5]
+    gt = api.DeviceModel(ctx, fp32_exact(orc.ground_truth_model(pts, cols, 0.01)))
+    dviews = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), cams, pts, True, 2.0, 2.0)
+    seeds = api.seed_gaussians(pts, cols, 3, ctx=ctx).download()
+    cfg = TrainConfig(iterations=9, seed=4, densify_interval=0)
+    runs = []
+    dm = api.DeviceModel(ctx, seeds)
+    runs.append(api.train_device(dm, dviews, cfg, loss_trace=True)[1])
+    p0 = dm.download().params
+    planar = [dviews.download_planar(i, pin=True) for i in range(len(cams))]
+    hv = api.HostViews(ctx, dviews.cams, [g for g, _ in planar], [m for _, m in planar])
+    dm.upload(seeds)
+    runs.append(api.train_device(dm, hv, cfg, loss_trace=True)[1])
+    p1 = dm.download().params
+    tv = [dviews.download(i) for i in range(len(cams))]
+    r = api.train_partition_full(seeds, tv, cfg, ctx=ctx, loss_trace=True)
+    runs.append(r.loss_trace)
+    np.testing.assert_array_equal(runs[0], runs[1])
+    np.testing.assert_array_equal(runs[0], runs[2])
+    np.testing.assert_array_equal(p0, p1)
+    np.testing.assert_array_equal(p0, r.model.params)

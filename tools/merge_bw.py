@@ -52,7 +52,7 @@ def main():
             wire = 56.0 * n * (world - 1) / world
             print(f"rep {r}: {n:,} splats, {t.item():.2f} ms, {wire / (t.item() * 1e-3) / 1e9:.1f} GB/s "
                   f"into each GPU [{os.environ.get('NCCL_ALGO', '-')}/{os.environ.get('NCCL_PROTO', '-')}"
-                  f"/ch{os.environ.get('NCCL_MIN_NCHANNELS', '-')}/nvls{os.environ.get('NCCL_NVLS_ENABLE', '-')}]",
+                  f"/ch{os.environ.get('NCCL_MIN_NCHANNELS', '-')}] via {api.merge_exchange()}",
                   flush=True)
         del merged
     comm.close()
