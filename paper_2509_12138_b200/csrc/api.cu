@@ -1828,9 +1828,6 @@ int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* local
   });
 }
 
-namespace dsg {
-extern const char* g_merge_path;
-}
 const char* dsg_merge_exchange(void) { return dsg::g_merge_path; }
 
 int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,

@@ -240,6 +240,7 @@ DensifyResult densify_dev(ModelDev& m, ModelDev& spare, DensifyScratch& ds, doub
                           cudaStream_t st);
 
 // NCCL exchange (comm.cu): ghost-trim merge all-gather, band gather.
+extern const char* g_merge_path;  // last merge exchange: "peer" or "nccl"
 void nccl_unique_id(uint8_t out[128]);
 void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(void* comm);
