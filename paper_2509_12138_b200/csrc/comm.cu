@@ -16,6 +16,7 @@
 // already resident (e.g. torch's) instead of mapping a second copy.
 #include <dlfcn.h>
 #include <cstdlib>
+#include <cstring>
 #include <nccl.h>
 
 #include <string>
@@ -190,9 +191,11 @@ static bool merge_from_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
   }
   // publish the buffer; the all-gather completes only after every rank packed
   cudaIpcMemHandle_t mine;
+  std::memset(&mine, 0, sizeof mine);
+  bool ok = true;
   if (cudaIpcGetMemHandle(&mine, send.get()) != cudaSuccess) {
     cudaGetLastError();
-    return false;
+    ok = false;  // still take part in the collectives below: all ranks decide together
   }
   DevBuf<uint8_t> hbuf;
   hbuf.ensure((size_t)64 * (nranks + 1));
@@ -203,8 +206,7 @@ static bool merge_from_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
   // every rank's record offsets (the same padding rule, from the counts)
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
   std::vector<const float*> src(nranks, nullptr);
-  bool ok = true;
-  for (int r = 0; r < nranks; ++r) {
+  for (int r = 0; r < nranks && ok; ++r) {
     if (r == rank) {
       src[r] = send.get();
       continue;
