@@ -140,86 +140,72 @@ __global__ void k_unpack_records(const float* __restrict__ rec, int64_t maxc, in
   if (i >= cnt[r]) return;  // padding
   P[k * pitch + off[r] + i] = rec[t];
 }
-// One partition's packed records [cnt][14], read straight from the owning
-// GPU's memory over NVLink (CUDA IPC mapping), transposed through shared
-// memory into the merged planar store at `off`: the transfer and the layout
-// change are one kernel. Coalesced 16 B loads (records start 16 B aligned:
-// partitions are padded to an even count), coalesced plane stores.
-constexpr int kPeerRecs = 256;
-__global__ void __launch_bounds__(256) k_peer_unpack(const float* __restrict__ src, int64_t cnt,
-                                                     float* __restrict__ P, int64_t pitch,
-                                                     int64_t off) {
-  __shared__ float4 sm4[kPeerRecs * kParams / 4];
-  float* sm = reinterpret_cast<float*>(sm4);
-  const int64_t b0 = (int64_t)blockIdx.x * kPeerRecs;
-  const int nrec = (int)(cnt - b0 < kPeerRecs ? cnt - b0 : (int64_t)kPeerRecs);
-  const float4* s4 = reinterpret_cast<const float4*>(src + b0 * kParams);
-  const int nf4 = (nrec * kParams + 3) / 4;  // the source is padded to whole float4s
-  for (int i = threadIdx.x; i < nf4; i += blockDim.x) sm4[i] = s4[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < nrec * kParams; i += blockDim.x) {
-    const int c = i / nrec, r = i - c * nrec;
-    P[c * pitch + off + b0 + r] = sm[r * kParams + c];
-  }
+// Push one local partition's survivors (dense planar [14][cnt]) into every
+// rank's merged planar model at the partition's offset: blockIdx.y = the
+// destination rank, reached through its CUDA IPC mapping over NVLink.
+// Reads and writes are coalesced per plane; all destinations are written
+// concurrently, so every link carries traffic at once.
+__global__ void __launch_bounds__(256) k_peer_push(const float* __restrict__ dense, int64_t dpitch,
+                                                   int64_t cnt, float* const* __restrict__ dst,
+                                                   const int64_t* __restrict__ dst_pitch,
+                                                   int64_t off) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  float* d = dst[blockIdx.y];
+  const int64_t pitch = dst_pitch[blockIdx.y];
+#pragma unroll
+  for (int c = 0; c < kParams; ++c) d[c * pitch + off + i] = __ldg(dense + c * dpitch + i);
 }
 }  // namespace
 
 // Peer-memory variant of step 3 (default; DSG_MERGE_PATH=nccl selects the
-// all-gather): every rank packs all its partitions' survivors into one
-// buffer, publishes its CUDA IPC handle (an all-gather of 64 B handles,
-// which also orders it after every rank's packing), and then pulls each
-// partition's records from the owning GPU with k_peer_unpack — NVLink reads
-// and the planar scatter in one pass. An all-reduce of one word after the
-// pulls tells every rank its buffer is no longer read.
-static bool merge_from_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
+// all-gather): every rank publishes the CUDA IPC handle and pitch of its
+// merged model's parameter store (a 72 B all-gather), maps the others', and
+// pushes each of its partitions' survivors straight into every rank's merged
+// model at the partition's offset (k_peer_push) — the transfer and the
+// planar placement in one kernel, all destinations at once. A one-word
+// all-reduce after the pushes tells every rank its merged model is complete.
+static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
                              const std::vector<DevBuf<float>>& dense,
                              const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
                              ModelDev& merged, cudaStream_t st, float* wire_ms) {
-  const int P = nranks * nlocal;
-  // my partitions' records, each padded to an even count (16 B-aligned starts)
-  std::vector<int64_t> roff(nlocal + 1, 0);
-  for (int j = 0; j < nlocal; ++j) roff[j + 1] = roff[j] + ((cnt[j * nranks + rank] + 1) & ~int64_t(1));
-  DevBuf<float> send;
-  send.ensure((size_t)std::max<int64_t>(roff[nlocal], 2) * kParams + 4);
-  for (int j = 0; j < nlocal; ++j) {
-    const int64_t my = cnt[j * nranks + rank];
-    if (my > 0) {
-      k_pack_records<<<(unsigned)((my * kParams + 255) / 256), 256, 0, st>>>(
-          dense[j].get(), std::max<int64_t>(my, 1), my, send.get() + roff[j] * kParams);
-      count_launch();
-    }
-  }
-  // publish the buffer; the all-gather completes only after every rank packed
-  cudaIpcMemHandle_t mine;
+  struct Pub {
+    cudaIpcMemHandle_t h;
+    int64_t pitch;
+  };
+  static_assert(sizeof(Pub) == 72, "published record");
+  Pub mine;
   std::memset(&mine, 0, sizeof mine);
-  bool ok = true;
-  if (cudaIpcGetMemHandle(&mine, send.get()) != cudaSuccess) {
-    cudaGetLastError();
-    ok = false;  // still take part in the collectives below: all ranks decide together
-  }
-  DevBuf<uint8_t> hbuf;
-  hbuf.ensure((size_t)64 * (nranks + 1));
-  DSG_CUDA_CHECK(cudaMemcpyAsync(hbuf.get() + 64 * nranks, &mine, 64, cudaMemcpyHostToDevice, st));
-  nc(N.AllGather(hbuf.get() + 64 * nranks, hbuf.get(), 64, ncclUint8, c, st), "allgather handles");
-  std::vector<cudaIpcMemHandle_t> hs(nranks);
-  DSG_CUDA_CHECK(cudaMemcpyAsync(hs.data(), hbuf.get(), 64 * nranks, cudaMemcpyDeviceToHost, st));
-  // every rank's record offsets (the same padding rule, from the counts)
+  mine.pitch = merged.cap;
+  bool ok = cudaIpcGetMemHandle(&mine.h, merged.params.get()) == cudaSuccess;
+  if (!ok) cudaGetLastError();  // still take part in the collectives: all ranks decide together
+  DevBuf<uint8_t> pbuf;
+  pbuf.ensure(sizeof(Pub) * (nranks + 1));
+  DSG_CUDA_CHECK(cudaMemcpyAsync(pbuf.get() + sizeof(Pub) * nranks, &mine, sizeof(Pub),
+                                 cudaMemcpyHostToDevice, st));
+  nc(N.AllGather(pbuf.get() + sizeof(Pub) * nranks, pbuf.get(), sizeof(Pub), ncclUint8, c, st),
+     "allgather handles");
+  std::vector<Pub> pubs(nranks);
+  DSG_CUDA_CHECK(cudaMemcpyAsync(pubs.data(), pbuf.get(), sizeof(Pub) * nranks,
+                                 cudaMemcpyDeviceToHost, st));
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-  std::vector<const float*> src(nranks, nullptr);
-  for (int r = 0; r < nranks && ok; ++r) {
+  std::vector<float*> dst(nranks, nullptr);
+  std::vector<int64_t> pitch(nranks);
+  for (int r = 0; r < nranks; ++r) {
+    pitch[r] = pubs[r].pitch;
     if (r == rank) {
-      src[r] = send.get();
+      dst[r] = merged.params.get();
       continue;
     }
+    if (!ok) continue;
     void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    if (cudaIpcOpenMemHandle(&p, pubs[r].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       ok = false;
       continue;
     }
-    src[r] = static_cast<const float*>(p);
+    dst[r] = static_cast<float*>(p);
   }
-  // every rank must agree before anyone relies on peer reads
   DevBuf<int> flag;
   flag.ensure(1);
   const int okv = ok ? 1 : 0;
@@ -229,21 +215,28 @@ static bool merge_from_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
   DSG_CUDA_CHECK(cudaMemcpyAsync(&all_ok, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
   if (all_ok) {
+    DevBuf<float*> dptr;
+    DevBuf<int64_t> dpitch;
+    dptr.ensure(nranks);
+    dpitch.ensure(nranks);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(dptr.get(), dst.data(), sizeof(float*) * nranks,
+                                   cudaMemcpyHostToDevice, st));
+    DSG_CUDA_CHECK(cudaMemcpyAsync(dpitch.get(), pitch.data(), sizeof(int64_t) * nranks,
+                                   cudaMemcpyHostToDevice, st));
     cudaEvent_t e0, e1;
     DSG_CUDA_CHECK(cudaEventCreate(&e0));
     DSG_CUDA_CHECK(cudaEventCreate(&e1));
     DSG_CUDA_CHECK(cudaEventRecord(e0, st));
-    for (int k = 0; k < P; ++k) {  // partition order
-      const int r = k % nranks, j = k / nranks;
+    for (int j = 0; j < nlocal; ++j) {
+      const int k = j * nranks + rank;
       if (cnt[k] == 0) continue;
-      int64_t ro = 0;  // rank r's record offset of its j-th partition
-      for (int jj = 0; jj < j; ++jj) ro += (cnt[jj * nranks + r] + 1) & ~int64_t(1);
-      k_peer_unpack<<<(unsigned)((cnt[k] + kPeerRecs - 1) / kPeerRecs), 256, 0, st>>>(
-          src[r] + ro * kParams, cnt[k], merged.params.get(), merged.cap, off[k]);
+      const dim3 grid((unsigned)((cnt[k] + 255) / 256), (unsigned)nranks);
+      k_peer_push<<<grid, 256, 0, st>>>(dense[j].get(), std::max<int64_t>(cnt[k], 1), cnt[k],
+                                        dptr.get(), dpitch.get(), off[k]);
       count_launch();
     }
     DSG_CUDA_CHECK(cudaEventRecord(e1, st));
-    // nobody frees or reuses a buffer a peer may still be reading
+    // every rank's pushes have landed before anyone uses its merged model
     nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce done");
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
     float t = 0.f;
@@ -253,7 +246,7 @@ static bool merge_from_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
     if (wire_ms) *wire_ms = t;
   }
   for (int r = 0; r < nranks; ++r)
-    if (r != rank && src[r]) cudaIpcCloseMemHandle(const_cast<float*>(src[r]));
+    if (r != rank && dst[r]) cudaIpcCloseMemHandle(dst[r]);
   return all_ok != 0;
 }
 
@@ -318,7 +311,7 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* co
     return e && std::string(e) == "nccl";
   }();
   if (!use_nccl && nranks > 1 &&
-      merge_from_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms)) {
+      merge_push_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms)) {
     g_merge_path = "peer";
     return total;
   }
