@@ -156,6 +156,33 @@ __global__ void __launch_bounds__(256) k_peer_push(const float* __restrict__ den
 #pragma unroll
   for (int c = 0; c < kParams; ++c) d[c * pitch + off + i] = __ldg(dense + c * dpitch + i);
 }
+
+// Pull: one launch over every partition (blockIdx.y = partition k), each
+// block copying 256 records of partition k from the owning GPU's packed
+// buffer (CUDA IPC mapping, NVLink reads of 16 B) through shared memory into
+// the local merged planar store — all peers' links busy at once.
+constexpr int kPeerRecs = 256;
+struct PullPart {
+  const float* src;  // partition's first record on its owner
+  int64_t cnt, off;
+};
+__global__ void __launch_bounds__(256) k_peer_pull(const PullPart* __restrict__ parts,
+                                                   float* __restrict__ P, int64_t pitch) {
+  __shared__ float4 sm4[kPeerRecs * kParams / 4];
+  float* sm = reinterpret_cast<float*>(sm4);
+  const PullPart pp = parts[blockIdx.y];
+  const int64_t b0 = (int64_t)blockIdx.x * kPeerRecs;
+  if (b0 >= pp.cnt) return;
+  const int nrec = (int)(pp.cnt - b0 < kPeerRecs ? pp.cnt - b0 : (int64_t)kPeerRecs);
+  const float4* s4 = reinterpret_cast<const float4*>(pp.src + b0 * kParams);
+  const int nf4 = (nrec * kParams + 3) / 4;  // sources are padded to whole float4s
+  for (int i = threadIdx.x; i < nf4; i += blockDim.x) sm4[i] = s4[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < nrec * kParams; i += blockDim.x) {
+    const int c = i / nrec, r = i - c * nrec;
+    P[c * pitch + pp.off + b0 + r] = sm[r * kParams + c];
+  }
+}
 }  // namespace
 
 // Peer-memory variant of step 3 (default; DSG_MERGE_PATH=nccl selects the
@@ -250,6 +277,102 @@ static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
   return all_ok != 0;
 }
 
+// Pull variant: every rank packs its partitions' survivors into one buffer
+// of 56 B records (each partition padded to an even count, so record starts
+// are 16 B aligned), publishes its IPC handle, and pulls all partitions it
+// does not own with one k_peer_pull launch.
+static bool merge_pull_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
+                             const std::vector<DevBuf<float>>& dense,
+                             const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
+                             ModelDev& merged, cudaStream_t st, float* wire_ms) {
+  const int P = nranks * nlocal;
+  auto padded = [&](int k) { return (cnt[k] + 1) & ~int64_t(1); };
+  std::vector<int64_t> roff(P, 0);  // record offset of partition k in its owner's buffer
+  for (int r = 0; r < nranks; ++r) {
+    int64_t o = 0;
+    for (int j = 0; j < nlocal; ++j) {
+      roff[j * nranks + r] = o;
+      o += padded(j * nranks + r);
+    }
+  }
+  int64_t mine_recs = 0;
+  for (int j = 0; j < nlocal; ++j) mine_recs += padded(j * nranks + rank);
+  DevBuf<float> send;
+  send.ensure((size_t)std::max<int64_t>(mine_recs, 2) * kParams + 4);
+  for (int j = 0; j < nlocal; ++j) {
+    const int k = j * nranks + rank;
+    if (cnt[k] > 0) {
+      k_pack_records<<<(unsigned)((cnt[k] * kParams + 255) / 256), 256, 0, st>>>(
+          dense[j].get(), std::max<int64_t>(cnt[k], 1), cnt[k], send.get() + roff[k] * kParams);
+      count_launch();
+    }
+  }
+  cudaIpcMemHandle_t mine;
+  std::memset(&mine, 0, sizeof mine);
+  bool ok = cudaIpcGetMemHandle(&mine, send.get()) == cudaSuccess;
+  if (!ok) cudaGetLastError();
+  DevBuf<uint8_t> hbuf;
+  hbuf.ensure((size_t)64 * (nranks + 1));
+  DSG_CUDA_CHECK(cudaMemcpyAsync(hbuf.get() + 64 * nranks, &mine, 64, cudaMemcpyHostToDevice, st));
+  nc(N.AllGather(hbuf.get() + 64 * nranks, hbuf.get(), 64, ncclUint8, c, st), "allgather handles");
+  std::vector<cudaIpcMemHandle_t> hs(nranks);
+  DSG_CUDA_CHECK(cudaMemcpyAsync(hs.data(), hbuf.get(), 64 * nranks, cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::vector<const float*> src(nranks, nullptr);
+  for (int r = 0; r < nranks && ok; ++r) {
+    if (r == rank) {
+      src[r] = send.get();
+      continue;
+    }
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, hs[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = false;
+      continue;
+    }
+    src[r] = static_cast<const float*>(p);
+  }
+  DevBuf<int> flag;
+  flag.ensure(1);
+  const int okv = ok ? 1 : 0;
+  DSG_CUDA_CHECK(cudaMemcpyAsync(flag.get(), &okv, sizeof(int), cudaMemcpyHostToDevice, st));
+  nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce ipc status");
+  int all_ok = 0;
+  DSG_CUDA_CHECK(cudaMemcpyAsync(&all_ok, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (all_ok) {
+    std::vector<PullPart> pp(P);
+    int64_t maxc = 1;
+    for (int k = 0; k < P; ++k) {
+      const int r = k % nranks;
+      pp[k] = PullPart{src[r] + roff[k] * kParams, cnt[k], off[k]};
+      maxc = std::max(maxc, cnt[k]);
+    }
+    DevBuf<PullPart> dpp;
+    dpp.ensure(P);
+    DSG_CUDA_CHECK(cudaMemcpyAsync(dpp.get(), pp.data(), sizeof(PullPart) * P,
+                                   cudaMemcpyHostToDevice, st));
+    cudaEvent_t e0, e1;
+    DSG_CUDA_CHECK(cudaEventCreate(&e0));
+    DSG_CUDA_CHECK(cudaEventCreate(&e1));
+    DSG_CUDA_CHECK(cudaEventRecord(e0, st));
+    k_peer_pull<<<dim3((unsigned)((maxc + kPeerRecs - 1) / kPeerRecs), (unsigned)P), 256, 0, st>>>(
+        dpp.get(), merged.params.get(), merged.cap);
+    count_launch();
+    DSG_CUDA_CHECK(cudaEventRecord(e1, st));
+    nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce done");
+    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+    float t = 0.f;
+    DSG_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (wire_ms) *wire_ms = t;
+  }
+  for (int r = 0; r < nranks; ++r)
+    if (r != rank && src[r]) cudaIpcCloseMemHandle(const_cast<float*>(src[r]));
+  return all_ok != 0;
+}
+
 // Steps 1-3 above. `merged` receives the merged model (reserved inside).
 // Rank r holds partitions k = j * nranks + r for j < nlocal (partition k on
 // GPU k mod N, runtime.hpp:337-343 worker assignment). The survivors travel
@@ -306,13 +429,18 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* co
   merged.reserve(std::max<int64_t>(total, 1));
   merged.n = total;
   // 3a. peer-memory pull (default)
-  static const bool use_nccl = [] {
+  static const std::string path = [] {
     const char* e = std::getenv("DSG_MERGE_PATH");
-    return e && std::string(e) == "nccl";
+    return std::string(e ? e : "nccl");
   }();
-  if (!use_nccl && nranks > 1 &&
+  if (path == "pull" && nranks > 1 &&
+      merge_pull_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms)) {
+    g_merge_path = "pull";
+    return total;
+  }
+  if (path == "push" && nranks > 1 &&
       merge_push_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms)) {
-    g_merge_path = "peer";
+    g_merge_path = "push";
     return total;
   }
   g_merge_path = "nccl";
