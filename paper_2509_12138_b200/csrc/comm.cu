@@ -161,14 +161,17 @@ __global__ void __launch_bounds__(256) k_peer_push(const float* __restrict__ den
 // block copying 256 records of partition k from the owning GPU's packed
 // buffer (CUDA IPC mapping, NVLink reads of 16 B) through shared memory into
 // the local merged planar store — all peers' links busy at once.
-constexpr int kPeerRecs = 256;
+#ifndef DSG_PEER_RECS
+#define DSG_PEER_RECS 1024  // records per block: 14 float4 NVLink loads in flight per thread
+#endif
+constexpr int kPeerRecs = DSG_PEER_RECS;
 struct PullPart {
   const float* src;  // partition's first record on its owner
   int64_t cnt, off;
 };
 __global__ void __launch_bounds__(256) k_peer_pull(const PullPart* __restrict__ parts,
                                                    float* __restrict__ P, int64_t pitch) {
-  __shared__ float4 sm4[kPeerRecs * kParams / 4];
+  extern __shared__ float4 sm4[];  // kPeerRecs * kParams floats
   float* sm = reinterpret_cast<float*>(sm4);
   const PullPart pp = parts[blockIdx.y];
   const int64_t b0 = (int64_t)blockIdx.x * kPeerRecs;
@@ -176,7 +179,18 @@ __global__ void __launch_bounds__(256) k_peer_pull(const PullPart* __restrict__ 
   const int nrec = (int)(pp.cnt - b0 < kPeerRecs ? pp.cnt - b0 : (int64_t)kPeerRecs);
   const float4* s4 = reinterpret_cast<const float4*>(pp.src + b0 * kParams);
   const int nf4 = (nrec * kParams + 3) / 4;  // sources are padded to whole float4s
-  for (int i = threadIdx.x; i < nf4; i += blockDim.x) sm4[i] = s4[i];
+  constexpr int kPer = (kPeerRecs * kParams / 4 + 255) / 256;
+  float4 v[kPer];  // issue every load before the first store
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = threadIdx.x + u * 256;
+    if (i < nf4) v[u] = s4[i];
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const int i = threadIdx.x + u * 256;
+    if (i < nf4) sm4[i] = v[u];
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < nrec * kParams; i += blockDim.x) {
     const int c = i / nrec, r = i - c * nrec;
@@ -356,8 +370,11 @@ static bool merge_pull_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
     DSG_CUDA_CHECK(cudaEventCreate(&e0));
     DSG_CUDA_CHECK(cudaEventCreate(&e1));
     DSG_CUDA_CHECK(cudaEventRecord(e0, st));
-    k_peer_pull<<<dim3((unsigned)((maxc + kPeerRecs - 1) / kPeerRecs), (unsigned)P), 256, 0, st>>>(
-        dpp.get(), merged.params.get(), merged.cap);
+    const size_t smem = sizeof(float) * kPeerRecs * kParams;
+    DSG_CUDA_CHECK(cudaFuncSetAttribute(k_peer_pull, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+    k_peer_pull<<<dim3((unsigned)((maxc + kPeerRecs - 1) / kPeerRecs), (unsigned)P), 256, smem,
+                  st>>>(dpp.get(), merged.params.get(), merged.cap);
     count_launch();
     DSG_CUDA_CHECK(cudaEventRecord(e1, st));
     nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce done");
