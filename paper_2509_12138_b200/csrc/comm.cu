@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(256) k_peer_pull(const PullPart* __restrict__ 
 static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
                              const std::vector<DevBuf<float>>& dense,
                              const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
-                             ModelDev& merged, cudaStream_t st, float* wire_ms) {
+                             ModelDev& merged, cudaStream_t st, float* wire_ms,
+                             bool copy_engines = false) {
   struct Pub {
     cudaIpcMemHandle_t h;
     int64_t pitch;
@@ -268,15 +269,46 @@ static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
     DSG_CUDA_CHECK(cudaEventCreate(&e0));
     DSG_CUDA_CHECK(cudaEventCreate(&e1));
     DSG_CUDA_CHECK(cudaEventRecord(e0, st));
-    for (int j = 0; j < nlocal; ++j) {
-      const int k = j * nranks + rank;
-      if (cnt[k] == 0) continue;
-      const dim3 grid((unsigned)((cnt[k] + 255) / 256), (unsigned)nranks);
-      k_peer_push<<<grid, 256, 0, st>>>(dense[j].get(), std::max<int64_t>(cnt[k], 1), cnt[k],
-                                        dptr.get(), dpitch.get(), off[k]);
-      count_launch();
+    if (copy_engines) {
+      // plane segments copied by the copy engines, one stream per destination
+      std::vector<cudaStream_t> ss(nranks);
+      std::vector<cudaEvent_t> done(nranks);
+      for (int r = 0; r < nranks; ++r) {
+        DSG_CUDA_CHECK(cudaStreamCreateWithFlags(&ss[r], cudaStreamNonBlocking));
+        DSG_CUDA_CHECK(cudaEventCreateWithFlags(&done[r], cudaEventDisableTiming));
+        DSG_CUDA_CHECK(cudaStreamWaitEvent(ss[r], e0, 0));
+      }
+      for (int j = 0; j < nlocal; ++j) {
+        const int k = j * nranks + rank;
+        if (cnt[k] == 0) continue;
+        for (int r = 0; r < nranks; ++r)
+          for (int ch = 0; ch < kParams; ++ch)
+            DSG_CUDA_CHECK(cudaMemcpyAsync(dst[r] + ch * pitch[r] + off[k],
+                                           dense[j].get() + ch * std::max<int64_t>(cnt[k], 1),
+                                           sizeof(float) * cnt[k], cudaMemcpyDeviceToDevice,
+                                           ss[r]));
+      }
+      for (int r = 0; r < nranks; ++r) {
+        DSG_CUDA_CHECK(cudaEventRecord(done[r], ss[r]));
+        DSG_CUDA_CHECK(cudaStreamWaitEvent(st, done[r], 0));
+      }
+      DSG_CUDA_CHECK(cudaEventRecord(e1, st));
+      DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+      for (int r = 0; r < nranks; ++r) {
+        cudaEventDestroy(done[r]);
+        cudaStreamDestroy(ss[r]);
+      }
+    } else {
+      for (int j = 0; j < nlocal; ++j) {
+        const int k = j * nranks + rank;
+        if (cnt[k] == 0) continue;
+        const dim3 grid((unsigned)((cnt[k] + 255) / 256), (unsigned)nranks);
+        k_peer_push<<<grid, 256, 0, st>>>(dense[j].get(), std::max<int64_t>(cnt[k], 1), cnt[k],
+                                          dptr.get(), dpitch.get(), off[k]);
+        count_launch();
+      }
+      DSG_CUDA_CHECK(cudaEventRecord(e1, st));
     }
-    DSG_CUDA_CHECK(cudaEventRecord(e1, st));
     // every rank's pushes have landed before anyone uses its merged model
     nc(N.AllReduce(flag.get(), flag.get(), 1, ncclInt32, ncclMin, c, st), "allreduce done");
     DSG_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -458,6 +490,11 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* co
   if (path == "push" && nranks > 1 &&
       merge_push_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms)) {
     g_merge_path = "push";
+    return total;
+  }
+  if (path == "copy" && nranks > 1 &&
+      merge_push_peers(N, c, nranks, rank, nlocal, dense, cnt, off, merged, st, wire_ms, true)) {
+    g_merge_path = "copy";
     return total;
   }
   g_merge_path = "nccl";
