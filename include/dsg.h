@@ -285,11 +285,12 @@ int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* local
                               int32_t nlocal, int32_t axis, const double* cut_lo,
                               const double* cut_hi, dsg_model merged, int64_t* n_merged,
                               double* ms);
-/* How the last merge moved the survivors: "peer" (each GPU pulls the other
- * GPUs' packed records over NVLink through CUDA IPC mappings, transposing
- * them into its merged model in the same kernel; the default) or "nccl" (one
- * NCCL all-gather per partition round; DSG_MERGE_PATH=nccl, or the fallback
- * when IPC is unavailable). */
+/* How the last merge moved the survivors: "nccl" (one NCCL all-gather of
+ * packed records per partition round; the default) or, selected with
+ * DSG_MERGE_PATH, "pull" / "push" / "copy" (CUDA IPC mappings of the peers'
+ * buffers: NVLink reads with an in-kernel transpose, NVLink writes, or
+ * copy-engine plane copies); a peer variant falls back to NCCL when IPC is
+ * unavailable. */
 const char* dsg_merge_exchange(void);
 /* Tile-parallel render (comm may be NULL): rank r bins and blends tile-row
  * band r of the replicated model, the bands cut at the quantiles of the

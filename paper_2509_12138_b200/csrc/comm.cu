@@ -6,9 +6,10 @@
 //      rule, partition.hpp:120) on the device;
 //   2. the survivor counts are all-gathered (int64);
 //   3. the survivors are all-gathered as packed 56 B records (one NCCL
-//      all-gather, padded to the largest slab) and scattered into one merged
-//      planar model in (partition, index) order — merge_models' order
-//      (partition.hpp:117-123) — so every GPU holds the merged model;
+//      all-gather per partition round, padded to the largest slab) and
+//      scattered into one merged planar model in (partition, index) order —
+//      merge_models' order (partition.hpp:117-123) — so every GPU holds the
+//      merged model (peer-memory pull / push / copy variants beside it);
 //   4. the merged model is rendered tile-parallel: rank r bins and blends
 //      only its band of tile rows (preprocess is replicated), and the bands
 //      are gathered to rank 0 with ncclSend/ncclRecv.
@@ -199,13 +200,15 @@ __global__ void __launch_bounds__(256) k_peer_pull(const PullPart* __restrict__ 
 }
 }  // namespace
 
-// Peer-memory variant of step 3 (default; DSG_MERGE_PATH=nccl selects the
-// all-gather): every rank publishes the CUDA IPC handle and pitch of its
-// merged model's parameter store (a 72 B all-gather), maps the others', and
-// pushes each of its partitions' survivors straight into every rank's merged
-// model at the partition's offset (k_peer_push) — the transfer and the
-// planar placement in one kernel, all destinations at once. A one-word
-// all-reduce after the pushes tells every rank its merged model is complete.
+// Peer-memory variants of step 3 (DSG_MERGE_PATH=push / copy; the NCCL
+// all-gather is the default, measured fastest on the 4-GPU box: DESIGN §7):
+// every rank publishes the CUDA IPC handle and pitch of its merged model's
+// parameter store (a 72 B all-gather), maps the others', and pushes each of
+// its partitions' survivors straight into every rank's merged model at the
+// partition's offset — k_peer_push (the transfer and the planar placement in
+// one kernel, all destinations at once) or copy-engine plane copies. A
+// one-word all-reduce after the pushes tells every rank its merged model is
+// complete.
 static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
                              const std::vector<DevBuf<float>>& dense,
                              const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
