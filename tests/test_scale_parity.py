@@ -153,3 +153,28 @@ def test_config3_rt_partition_mask_and_step(ctx, ref, rt_cloud):
     rep["owned"], rep["ghosts"] = int(len(part.owned_indices)), int(len(part.ghost_indices))
     _record("config3_step", rep)
     _assert_pass(rep)
+
+
+def test_config2_three_step_trajectory(ctx, ref):
+    """Three training iterations of the benched 4M partition (trainer.hpp:
+    173-207: seeded view order, lr_mu decay, Adam) on three of its 1024^2
+    views, on both sides: the loss trace agrees to 1e-4 relative. Step 1
+    sees identical inputs; later steps see the fp32 post-Adam parameters,
+    whose only visible differences are the noise-level gradient components
+    where Adam's epsilon = 1e-15 moves a scalar by +-lr either way."""
+    import os as _os
+    pts, cols, _ = scenes.kingsnake(scenes.SIZES["kingsnake"], seed=1, turns=6.0)
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    rig = scenes.rig_for_cloud(pts, 28, 16, 1024)
+    from bench import split_rig
+    train_idx, _ = split_rig(len(rig), 0.1, 1)
+    cams = [rig[i] for i in train_idx[:3]]
+    gt = api.ground_truth_model(pts, cols, nn, 0.97, ctx=ctx)
+    views = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), cams, pts, True, 2.0, 2.0)
+    tv = [views.download(k) for k in range(3)]
+    seeds = SplatModel(np.ascontiguousarray(api.seed_gaussians(pts, cols, 3, ctx=ctx).download().params))
+    cfg = TrainConfig(iterations=3, seed=1)
+    a = api.train_partition_full(seeds, tv, cfg, ctx=ctx, loss_trace=True)
+    b = ref.train_partition_full(seeds, tv, cfg, shards=_os.cpu_count() or 1, loss_trace=True)
+    _record("config2_trajectory", {"device": a.loss_trace.tolist(), "reference": b.loss_trace.tolist()})
+    np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=1e-4)
