@@ -628,9 +628,14 @@ def render_timed(dmodel: DeviceModel, cams, cfg: RenderConfig, repeats: int = 1)
 
 
 def pinned(a: np.ndarray) -> np.ndarray:
-    """Page-lock a numpy array in place (kept registered for its lifetime)."""
+    """Page-lock a numpy array in place; the registration is dropped when the
+    array is freed (a stale registration would make later copies into the
+    same address range fail)."""
+    import weakref
     a = np.ascontiguousarray(a)
-    _check(lib().dsg_host_register(C.c_void_p(a.ctypes.data), C.c_int64(a.nbytes)))
+    ptr = a.ctypes.data
+    _check(lib().dsg_host_register(C.c_void_p(ptr), C.c_int64(a.nbytes)))
+    weakref.finalize(a, lib().dsg_host_unregister, C.c_void_p(ptr))
     return a
 
 

@@ -133,9 +133,11 @@ int guarded(F&& f) {
     return 0;
   } catch (const Error& e) {
     g_err = std::string(kCodeNames[e.code]) + ": " + e.msg;
+    cudaGetLastError();  // a reported CUDA error must not resurface in the next call
     return e.code + 1;
   } catch (const std::exception& e) {
     g_err = std::string("InvalidArgument: ") + e.what();
+    cudaGetLastError();
     return kInvalidArgument + 1;
   }
 }

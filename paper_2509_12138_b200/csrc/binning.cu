@@ -33,6 +33,7 @@ namespace {
 #define DSG_PRE_MINB 5  // 5 CTAs/SM (48 regs): measured 0.27 vs 0.30 ms
 #endif
 __global__ void __launch_bounds__(256, DSG_PRE_MINB) k_preprocess(PreprocessArgs a) {
+  DSG_PDL_ENTRY();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   bool vis = false;
@@ -155,6 +156,7 @@ __global__ void k_vis_compact(const uint32_t* __restrict__ tcount, const double*
                               const unsigned long long* __restrict__ drange,
                               const uint32_t* __restrict__ slot, int64_t n,
                               uint32_t* __restrict__ vis_key, uint32_t* __restrict__ vis_idx) {
+  DSG_PDL_ENTRY();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n || tcount[i] == 0) return;
   const double lo = __longlong_as_double((long long)drange[0]);
@@ -181,6 +183,7 @@ __device__ __forceinline__ bool depth_before(uint32_t u, uint32_t v, const doubl
 __global__ void k_depth_mark(const uint32_t* __restrict__ key, const uint32_t* __restrict__ idx,
                              int64_t n, const double* __restrict__ depth,
                              uint32_t* __restrict__ runflag) {
+  DSG_PDL_ENTRY();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s + 1 >= n) return;
   const uint32_t k = key[s];
@@ -196,6 +199,7 @@ __global__ void k_depth_fixup(const uint32_t* __restrict__ key, uint32_t* idx, i
                               const double* __restrict__ depth,
                               const uint32_t* __restrict__ runflag, uint32_t* long_runs,
                               uint32_t long_cap) {
+  DSG_PDL_ENTRY();
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= n || !runflag[s]) return;
   const uint32_t k = key[s];
@@ -234,6 +238,7 @@ __global__ void k_run_keys(const uint32_t* __restrict__ idx, uint32_t s, uint32_
 
 __global__ void k_gather_counts(const uint32_t* __restrict__ vis_idx, int64_t nv,
                                 const uint32_t* __restrict__ tcount, uint32_t* out) {
+  DSG_PDL_ENTRY();
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s < nv) out[s] = tcount[vis_idx[s]];
 }
@@ -310,6 +315,7 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
                             const float4* __restrict__ mrow, bool rows, int tiles_x, int band_ty0,
                             int band_ty1, uint32_t* __restrict__ tile_key,
                             uint32_t* __restrict__ dup_val, uint32_t* __restrict__ dup_base) {
+  DSG_PDL_ENTRY();
   int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nv) return;
   uint32_t i = vis_idx[s];
@@ -346,6 +352,7 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
 // for the blend warps).
 __global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd, uint2* ranges,
                               uint8_t* __restrict__ emask) {
+  DSG_PDL_ENTRY();
   // four entries per thread: one 16 B key load, one 4 B mask store
   const int64_t e0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (e0 >= nd) return;
@@ -383,6 +390,7 @@ __global__ void k_tile_ranges(const uint32_t* __restrict__ tile_key, int64_t nd,
 // background); units of a tile are consecutive.
 __global__ void k_unit_counts(const uint2* __restrict__ ranges, const uint32_t* __restrict__ order,
                               int nt, uint32_t seg, uint32_t* __restrict__ cnt) {
+  DSG_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint2 r = ranges[order[i]];
@@ -396,6 +404,7 @@ __global__ void k_unit_fill(const uint2* __restrict__ ranges, const uint32_t* __
                             int nt, uint32_t seg, uint32_t split_len,
                             const uint32_t* __restrict__ base,
                             uint4* __restrict__ units, uint32_t* __restrict__ first_of) {
+  DSG_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint32_t t = order[i];
@@ -421,6 +430,7 @@ constexpr int kBins = 4 * 32 + 2;
 
 __global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, uint32_t split,
                             uint32_t* bins, uint32_t* counts) {
+  DSG_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   const uint2 r = ranges[t0 + i];
@@ -437,7 +447,8 @@ __global__ void k_tile_bins(const uint2* __restrict__ ranges, int t0, int nt, ui
   atomicAdd(&counts[b], 1u);
 }
 
-__global__ void k_tile_bin_offsets(uint32_t* counts) {  // one warp: descending exclusive scan
+__global__ void k_tile_bin_offsets(uint32_t* counts) {
+  DSG_PDL_ENTRY();  // one warp: descending exclusive scan
   const int lane = threadIdx.x;
   uint32_t run = 0;
   for (int b = kBins - 1; b >= 0; --b) {
@@ -449,6 +460,7 @@ __global__ void k_tile_bin_offsets(uint32_t* counts) {  // one warp: descending 
 
 __global__ void k_tile_order(const uint32_t* __restrict__ bins, int t0, int nt, uint32_t* counts,
                              uint32_t* order) {
+  DSG_PDL_ENTRY();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nt) return;
   order[atomicAdd(&counts[bins[i]], 1u)] = (uint32_t)(t0 + i);
@@ -540,11 +552,11 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     a.depth = f.depth.get();
     a.exact = f.exact.get();
     a.drange = f.drange.get();
-    k_preprocess<<<blocks(n, 256), 256, 0, st>>>(a);
+    pdl_launch(k_preprocess, blocks(n, 256), 256, 0, st, a);
     count_launch();
     DSG_CUDA_CHECK(cudaGetLastError());
     exclusive_scan_u32(f.tcount.get(), f.vslot.get(), n, f.scan, st, true);
-    k_vis_compact<<<blocks(n, 256), 256, 0, st>>>(f.tcount.get(), f.depth.get(), f.drange.get(),
+    pdl_launch(k_vis_compact, blocks(n, 256), 256, 0, st, f.tcount.get(), f.depth.get(), f.drange.get(),
                                                   f.vslot.get(), n, f.vis_key.get(),
                                                   f.vis_idx.get());
     count_launch();
@@ -568,15 +580,15 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   constexpr uint32_t kLongCap = 1024;
   uint32_t* long_runs = f.long_runs.ensure(1 + 2 * kLongCap);
   DSG_CUDA_CHECK(cudaMemsetAsync(long_runs, 0, sizeof(uint32_t), st));
-  k_depth_mark<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get(), runflag);
-  k_depth_fixup<<<blocks(nv, 256), 256, 0, st>>>(skey, sidx, nv, f.depth.get(), runflag,
+  pdl_launch(k_depth_mark, blocks(nv, 256), 256, 0, st, skey, sidx, nv, f.depth.get(), runflag);
+  pdl_launch(k_depth_fixup, blocks(nv, 256), 256, 0, st, skey, sidx, nv, f.depth.get(), runflag,
                                                  long_runs, kLongCap);
   count_launch(2);
   tm.mark(2, st);
   f.sorted_idx = sidx;
   // per-splat tile counts in depth order, exclusive scan -> duplicate slots
   uint32_t* cnt = alt ? f.vis_key.get() : f.vis_key2.get();  // free buffer
-  k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+  pdl_launch(k_gather_counts, blocks(nv, 256), 256, 0, st, sidx, nv, f.tcount.get(), cnt);
   count_launch();
   exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
   uint32_t nd = 0, n_long = 0;
@@ -591,7 +603,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     // index-ordered compaction breaks ties by index.
     unsigned long long* rk = f.run_keys.ensure(2 * (size_t)nv);
     uint32_t* rv = f.run_vals.ensure(2 * (size_t)nv);
-    k_vis_compact<<<blocks(n, 256), 256, 0, st>>>(f.tcount.get(), f.depth.get(), f.drange.get(),
+    pdl_launch(k_vis_compact, blocks(n, 256), 256, 0, st, f.tcount.get(), f.depth.get(), f.drange.get(),
                                                   f.vslot.get(), n, cnt, rv);
     k_run_keys<<<blocks(nv, 256), 256, 0, st>>>(rv, 0, (uint32_t)nv, f.depth.get(), rk, rv + nv);
     count_launch(2);
@@ -600,7 +612,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
         64, f.sort, st);
     DSG_CUDA_CHECK(cudaMemcpyAsync(sidx, in_alt ? rv : rv + nv, sizeof(uint32_t) * nv,
                                    cudaMemcpyDeviceToDevice, st));
-    k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+    pdl_launch(k_gather_counts, blocks(nv, 256), 256, 0, st, sidx, nv, f.tcount.get(), cnt);
     count_launch();
     exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
   } else if (n_long > 0) {
@@ -622,7 +634,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
       DSG_CUDA_CHECK(cudaMemcpyAsync(sidx + s0, in_alt ? rv + len : rv, sizeof(uint32_t) * len,
                                      cudaMemcpyDeviceToDevice, st));
     }
-    k_gather_counts<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.tcount.get(), cnt);
+    pdl_launch(k_gather_counts, blocks(nv, 256), 256, 0, st, sidx, nv, f.tcount.get(), cnt);
     count_launch();
     exclusive_scan_u32(cnt, f.offs.get(), nv, f.scan, st);
   }
@@ -632,7 +644,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.tile_key2.ensure(std::max<uint32_t>(nd, 1));
   f.dup_val2.ensure(std::max<uint32_t>(nd, 1));
   if (f.tiles > (int64_t)kTileIdMask) fail(kInvalidArgument, "image has too many tiles");
-  k_duplicate<<<blocks(nv, 256), 256, 0, st>>>(sidx, nv, f.offs.get(), f.trect.get(),
+  pdl_launch(k_duplicate, blocks(nv, 256), 256, 0, st, sidx, nv, f.offs.get(), f.trect.get(),
                                                f.erect.get(), f.rec.get(), f.mrow.get(),
                                                g_exact_masks.load() != 0,
                                                cam.tiles_x, cam.band_ty0, cam.band_ty1,
@@ -647,7 +659,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.sorted_tile = alt2 ? f.tile_key2.get() : f.tile_key.get();
   f.sorted_val = alt2 ? f.dup_val2.get() : f.dup_val.get();
   f.emask.ensure(std::max<uint32_t>(nd, 1));
-  k_tile_ranges<<<blocks((nd + 3) / 4, 256), 256, 0, st>>>(f.sorted_tile, nd, f.ranges.get(),
+  pdl_launch(k_tile_ranges, blocks((nd + 3) / 4, 256), 256, 0, st, f.sorted_tile, nd, f.ranges.get(),
                                                  f.emask.get());
   count_launch();
   {
@@ -683,10 +695,10 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     }();
     if (split_env > 0) f.split_len = std::max<int64_t>(split_env, f.seg_len);
     f.split_cap = (int64_t)nd > f.split_len ? (int64_t)nd / f.split_len + 1 : 0;
-    k_tile_bins<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), t0, nt, (uint32_t)f.split_len,
+    pdl_launch(k_tile_bins, blocks(nt, 256), 256, 0, st, f.ranges.get(), t0, nt, (uint32_t)f.split_len,
                                                  f.tile_bins.get(), counts);
-    k_tile_bin_offsets<<<1, 32, 0, st>>>(counts);
-    k_tile_order<<<blocks(nt, 256), 256, 0, st>>>(f.tile_bins.get(), t0, nt, counts,
+    pdl_launch(k_tile_bin_offsets, 1, 32, 0, st, counts);
+    pdl_launch(k_tile_order, blocks(nt, 256), 256, 0, st, f.tile_bins.get(), t0, nt, counts,
                                                   f.tile_order.get());
     count_launch(3);
     // blend work units: ceil(len / seg_len) per tile in that order
@@ -697,11 +709,11 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     f.nonlast.ensure(std::max<int64_t>(f.unit_cap - nt, 1));
     f.ubuf.ensure((size_t)kUnitPlanes * f.unit_cap * kTile * kTile);
     uint32_t* ucnt = f.tile_bins.get();  // bins are consumed by k_tile_order
-    k_unit_counts<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), f.tile_order.get(), nt,
+    pdl_launch(k_unit_counts, blocks(nt, 256), 256, 0, st, f.ranges.get(), f.tile_order.get(), nt,
                                                    (uint32_t)f.seg_len, ucnt);
     count_launch();
     exclusive_scan_u32(ucnt, f.unit_base.get(), nt, f.scan, st);
-    k_unit_fill<<<blocks(nt, 256), 256, 0, st>>>(f.ranges.get(), f.tile_order.get(), nt,
+    pdl_launch(k_unit_fill, blocks(nt, 256), 256, 0, st, f.ranges.get(), f.tile_order.get(), nt,
                                                  (uint32_t)f.seg_len, (uint32_t)f.split_len,
                                                  f.unit_base.get(),
                                                  f.units.get(), f.nonlast.get());

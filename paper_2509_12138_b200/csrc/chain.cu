@@ -53,6 +53,7 @@ __device__ __forceinline__ void mm3(const Real* a, const Real* b, Real* r) {
 #define DSG_CHAIN_MINB 4  // 4 CTAs/SM (64 regs, 72 B spill): 0.34 vs 0.49 ms unbounded
 #endif
 __global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
+  DSG_PDL_ENTRY();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   double acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
 
 void chain_3d(const ChainArgs& a, cudaStream_t st) {
   if (a.n == 0) return;
-  k_chain<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a);
+  pdl_launch(k_chain, (unsigned)((a.n + 255) / 256), 256, 0, st, a);
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }

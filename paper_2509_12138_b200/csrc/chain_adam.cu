@@ -26,6 +26,7 @@ namespace {
 #define DSG_ADAM_MINB 1
 #endif
 __global__ void __launch_bounds__(256, DSG_ADAM_MINB) k_adam(AdamArgs a) {
+  DSG_PDL_ENTRY();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
   const int64_t P = a.pitch;
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(256, DSG_ADAM_MINB) k_adam(AdamArgs a) {
 
 void adam_update(const AdamArgs& a, cudaStream_t st) {
   if (a.n == 0) return;
-  k_adam<<<(unsigned)((a.n + 255) / 256), 256, 0, st>>>(a);
+  pdl_launch(k_adam, (unsigned)((a.n + 255) / 256), 256, 0, st, a);
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }

@@ -163,3 +163,45 @@ struct AlphaEval {
 namespace dsg {
 [[noreturn]] void throw_cuda(cudaError_t e, const char* expr, const char* file, int line);
 }
+
+// ---- programmatic dependent launch (sm_90+; used on the per-step path) -----
+// Every per-step kernel is launched with programmatic stream serialization
+// and starts with DSG_PDL_ENTRY(): it waits for its predecessor grid to
+// complete (and its writes to be visible) before touching memory, then lets
+// its own successor launch as soon as all of its blocks are resident, so the
+// successor's launch and block scheduling overlap this grid's tail instead
+// of following it.
+#ifndef DSG_NO_PDL
+#define DSG_PDL_ENTRY()                                   \
+  do {                                                    \
+    asm volatile("griddepcontrol.wait;" ::: "memory");    \
+    asm volatile("griddepcontrol.launch_dependents;" ::); \
+  } while (0)
+#else  // A/B builds without PDL
+#define DSG_PDL_ENTRY() \
+  do {                  \
+  } while (0)
+#endif
+
+namespace dsg {
+void count_launch(int n);
+template <class... KArgs, class... Args>
+inline void pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+#ifndef DSG_NO_PDL
+  cfg.numAttrs = 1;
+#else
+  cfg.numAttrs = 0;
+#endif
+  DSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...));
+}
+}  // namespace dsg

@@ -65,6 +65,7 @@ struct LossArgs {
 };
 
 __global__ void __launch_bounds__(kB* kB) k_ssim_stats(LossArgs a) {
+  DSG_PDL_ENTRY();
   __shared__ double xs[kE][kE], ys[kE][kE];
   __shared__ double hs[5][kE][kB];
   __shared__ double red[32];
@@ -159,6 +160,7 @@ __global__ void __launch_bounds__(kB* kB) k_ssim_stats(LossArgs a) {
 }
 
 __global__ void __launch_bounds__(kB* kB) k_loss_grad(LossArgs a) {
+  DSG_PDL_ENTRY();
   __shared__ double ps[3][kE][kE];
   __shared__ double hs[3][kE][kB];
   __shared__ double red[32];
@@ -233,6 +235,7 @@ __global__ void __launch_bounds__(kB* kB) k_loss_grad(LossArgs a) {
 }
 
 __global__ void __launch_bounds__(256) k_loss_final(LossArgs a) {
+  DSG_PDL_ENTRY();
   __shared__ double red[32];
   double s = 0.0, l = 0.0;
   // fixed per-thread strided order, then fixed tree: deterministic
@@ -329,11 +332,11 @@ void masked_loss_dev(Frame& f, const float* gt, const uint8_t* mask, int width, 
   a.loss_out = out ? out : f.loss_out.get();
   a.nblocks = nblocks;
   fill_window(a.win);
-  k_ssim_stats<<<grid, kB * kB, 0, st>>>(a);
+  pdl_launch(k_ssim_stats, grid, kB * kB, 0, st, a);
   count_launch();
-  k_loss_grad<<<grid, kB * kB, 0, st>>>(a);
+  pdl_launch(k_loss_grad, grid, kB * kB, 0, st, a);
   count_launch();
-  k_loss_final<<<1, 256, 0, st>>>(a);
+  pdl_launch(k_loss_final, 1, 256, 0, st, a);
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
@@ -364,7 +367,7 @@ void image_metrics_dev(Frame& f, const float* x, const float* y, int width, int 
   a.loss_out = out;
   a.nblocks = nblocks;
   fill_window(a.win);
-  k_ssim_stats<<<grid, kB * kB, 0, st>>>(a);
+  pdl_launch(k_ssim_stats, grid, kB * kB, 0, st, a);
   k_sq_err<<<grid, kB * kB, 0, st>>>(a);
   k_metric_final<<<1, 256, 0, st>>>(a);
   count_launch(3);

@@ -46,6 +46,7 @@ template <class K>
 __global__ void __launch_bounds__(256) k_digit_hist(const K* __restrict__ keys, int64_t n,
                                                     int begin_bit, int passes,
                                                     uint32_t* __restrict__ ghist) {
+  DSG_PDL_ENTRY();
   // 4 copies (one per warp pair) of up to 8 passes x 256 bins. Each thread
   // counts runs of equal digits in registers and flushes a run with one
   // shared atomic: high digits of sort keys are nearly constant, so this
@@ -110,6 +111,7 @@ scalar:
 
 // Exclusive scan of each pass's 256 bins (one block per pass).
 __global__ void k_hist_scan(uint32_t* ghist) {
+  DSG_PDL_ENTRY();
   __shared__ uint32_t tmp[33];
   uint32_t* h = ghist + blockIdx.x * kRadix;
   uint32_t agg;
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, int64_t n, int shift,
     const uint32_t* __restrict__ gscan, uint32_t* status, uint32_t* counter) {
+  DSG_PDL_ENTRY();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem<K>& sm = *reinterpret_cast<OnesweepSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -250,6 +253,7 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __restrict__ in,
                                                               int64_t n, uint32_t* sums,
                                                               bool flags) {
+  DSG_PDL_ENTRY();
   __shared__ uint32_t tmp[33];
   int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const uint32_t* __
 }
 
 __global__ void __launch_bounds__(1024) k_scan_sums(uint32_t* sums, int64_t nb) {
+  DSG_PDL_ENTRY();
   __shared__ uint32_t tmp[33];
   __shared__ uint32_t carry;
   if (threadIdx.x == 0) carry = 0;
@@ -285,6 +290,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __re
                                                             uint32_t* out, int64_t n,
                                                             const uint32_t* __restrict__ sums,
                                                             bool flags) {
+  DSG_PDL_ENTRY();
   __shared__ uint32_t tmp[33];
   int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
@@ -319,11 +325,11 @@ void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratc
   }
   int64_t nb = (n + kScanTile - 1) / kScanTile;
   uint32_t* sums = s.block_sums.ensure(nb + 1);
-  k_scan_reduce<<<(unsigned)nb, kScanThreads, 0, st>>>(in, n, sums, flags);
+  pdl_launch(k_scan_reduce, (unsigned)nb, kScanThreads, 0, st, in, n, sums, flags);
   count_launch();
-  k_scan_sums<<<1, 1024, 0, st>>>(sums, nb);
+  pdl_launch(k_scan_sums, 1, 1024, 0, st, sums, nb);
   count_launch();
-  k_scan_down<<<(unsigned)nb, kScanThreads, 0, st>>>(in, out, n, sums, flags);
+  pdl_launch(k_scan_down, (unsigned)nb, kScanThreads, 0, st, in, out, n, sums, flags);
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }
@@ -343,7 +349,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
   DSG_CUDA_CHECK(cudaMemsetAsync(status, 0, sizeof(uint32_t) * passes * parts * kRadix, st));
   DSG_CUDA_CHECK(cudaMemsetAsync(counters, 0, sizeof(uint32_t) * passes, st));
   int hist_blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-  k_digit_hist<K><<<hist_blocks, 256, 0, st>>>(keys, n, begin_bit, passes, hist);
+  pdl_launch(k_digit_hist<K>, hist_blocks, 256, 0, st, keys, n, begin_bit, passes, hist);
   count_launch();
   // Which digits actually vary? (a single populated bin = identity pass)
   std::vector<bool> trivial(passes, false);
@@ -356,7 +362,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
       for (int d = 0; d < kRadix; ++d)
         if (s.host_hist[(size_t)p * kRadix + d] == (uint32_t)n) trivial[p] = true;
   }
-  k_hist_scan<<<passes, kRadix, 0, st>>>(hist);
+  pdl_launch(k_hist_scan, passes, kRadix, 0, st, hist);
   count_launch();
   const size_t smem = sizeof(OnesweepSmem<K>);
   DSG_CUDA_CHECK(cudaFuncSetAttribute(k_onesweep<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -368,8 +374,7 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
     const uint32_t* vi = in_alt ? vals_alt : vals;
     K* ko = in_alt ? keys : keys_alt;
     uint32_t* vo = in_alt ? vals : vals_alt;
-    k_onesweep<K><<<(unsigned)parts, kSortThreads, smem, st>>>(
-        ki, vi, ko, vo, n, begin_bit + kRadixBits * p, hist + (size_t)p * kRadix,
+    pdl_launch(k_onesweep<K>, (unsigned)parts, kSortThreads, smem, st, ki, vi, ko, vo, n, begin_bit + kRadixBits * p, hist + (size_t)p * kRadix,
         status + (size_t)p * parts * kRadix, counters + p);
     count_launch();
     in_alt = !in_alt;
