@@ -379,3 +379,14 @@ def test_view_sources_train_identically(orc, ctx):
     np.testing.assert_array_equal(runs[0], runs[2])
     np.testing.assert_array_equal(p0, p1)
     np.testing.assert_array_equal(p0, r.model.params)
+
+
+def test_frame_work_counts_composited_pairs(ctx):
+    """dsg_frame_work: C = sum of n_contrib of the last forward (the blend
+    kernels' work count in the bench's roofline), plus the fix-up counters."""
+    m = fp32_exact(random_scene(99, 300))
+    m.params[:, 3:6] -= 1.5
+    r = api.render(m, make_camera(64), RenderConfig(), ctx=ctx)
+    w = api.frame_work(ctx)
+    assert w["composited"] == int(np.sum(r.per_pixel_contributor_count)) > 0
+    assert 0 <= w["term_changed"] <= w["term_fixups"]
