@@ -484,10 +484,10 @@ def partitioned_global(args, dist: Dist, ctx, work, parts, mine, pts, cols, nn, 
         merged, n_merged, wire_ms = api.merge_allgather_multi(comm, locs, [parts[k] for k in mine])
         merge_ms = dist.max(wire_ms)
     else:
-        api.merge_models(locs, [parts[k] for k in mine], ctx=ctx)  # allocation pass
+        merged = api.merge_models(locs, [parts[k] for k in mine], ctx=ctx)  # allocation pass
         ctx.synchronize()
         t0 = time.perf_counter()
-        merged = api.merge_models(locs, [parts[k] for k in mine], ctx=ctx)
+        merged = api.merge_models(locs, [parts[k] for k in mine], ctx=ctx, out=merged)
         merge_ms = (time.perf_counter() - t0) * 1e3
         n_merged = merged.info()[0]
     c0 = rig[0]

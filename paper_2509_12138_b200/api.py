@@ -671,8 +671,9 @@ def partition_cloud(positions, n: int, ghost_margin: float, ctx: Context = None)
     return parts
 
 
-def merge_models(models, partitions, ctx: Context = None) -> DeviceModel:
-    """merge_models (partition.hpp:109-126) over device models, one process."""
+def merge_models(models, partitions, ctx: Context = None, out: DeviceModel = None) -> DeviceModel:
+    """merge_models (partition.hpp:109-126) over device models, one process.
+    `out` (optional) is reused: its buffers are kept when large enough."""
     ctx = ctx or default_context()
     if len(models) != len(partitions):
         raise DsplatError(ErrorCode.MismatchedCounts, "one model per partition required")
@@ -680,7 +681,7 @@ def merge_models(models, partitions, ctx: Context = None) -> DeviceModel:
     arr = (C.c_void_p * len(dms))(*[d.h.value for d in dms])
     lo = np.array([p.cut_lo for p in partitions])
     hi = np.array([p.cut_hi for p in partitions])
-    out = DeviceModel(ctx)
+    out = out if out is not None else DeviceModel(ctx)
     _check(lib().dsg_merge_models(ctx.h, arr, C.c_int32(len(dms)),
                                   C.c_int32(partitions[0].cut_axis), _p(lo), _p(hi), out.h))
     return out

@@ -82,6 +82,7 @@ struct dsg_ctx_s {
   bool timer_init = false;
   ModelDev spare;  // densification output storage (swapped with the model's)
   DensifyScratch dscratch;
+  MergeScratch merge;  // ghost trim of merge_models / the merge exchange
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   // end-to-end mode: next step's view is copied on its own stream into the
   // other of two device slots while this step computes
@@ -1751,15 +1752,17 @@ int dsg_merge_models(dsg_ctx ctx, const dsg_model* models, int32_t nparts, int32
   return guarded([&] {  // merge_models (partition.hpp:109-126), single process
     DeviceGuard g(ctx->device);
     cudaStream_t st = ctx->stream;
-    std::vector<int64_t> cnt(nparts);
-    int64_t total = 0, it = 0;
+    std::vector<MergeSrc> src(nparts);
+    int64_t it = 0;
     for (int k = 0; k < nparts; ++k) {
       const ModelDev& m = models[k]->m;
-      cnt[k] = merge_compact_dev(m.params.get(), m.cap, m.n, axis, cut_lo[k], cut_hi[k], nullptr,
-                                 0, 0, ctx->frame.scan, st);
-      total += cnt[k];
+      src[k] = {m.params.get(), m.cap, m.n, cut_lo[k], cut_hi[k]};
       it = std::max(it, m.iteration);
     }
+    std::vector<int64_t> cnt(nparts);
+    merge_trim_count(src.data(), nparts, axis, ctx->merge, ctx->frame.scan, st, cnt.data());
+    int64_t total = 0;
+    for (int k = 0; k < nparts; ++k) total += cnt[k];
     ModelDev& o = out->m;
     o.reserve(std::max<int64_t>(total, 1));
     o.n = total;
@@ -1767,9 +1770,7 @@ int dsg_merge_models(dsg_ctx ctx, const dsg_model* models, int32_t nparts, int32
     o.origin_partition = -1;
     int64_t off = 0;
     for (int k = 0; k < nparts; ++k) {
-      const ModelDev& m = models[k]->m;
-      merge_compact_dev(m.params.get(), m.cap, m.n, axis, cut_lo[k], cut_hi[k], o.params.get(),
-                        o.cap, off, ctx->frame.scan, st);
+      merge_trim_scatter(src[k], k, ctx->merge, o.params.get(), o.cap, off, st);
       off += cnt[k];
     }
     reset_optimizer(ctx, o);
@@ -1820,7 +1821,8 @@ int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* local
     int64_t it_max = 0;
     const int64_t total = merge_allgather_dev(comm->nccl, comm->nranks, comm->rank, ms_.data(),
                                               nlocal, axis, cut_lo, cut_hi, merged->m,
-                                              ctx->frame.scan, ctx->stream, &t, &it_max);
+                                              ctx->frame.scan, ctx->merge, ctx->stream, &t,
+                                              &it_max);
     merged->m.iteration = it_max;  // merge_models: iteration = max (partition.hpp:124)
     merged->m.origin_partition = -1;
     reset_optimizer(ctx, merged->m);

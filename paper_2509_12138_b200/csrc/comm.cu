@@ -434,23 +434,27 @@ static bool merge_pull_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
 // into the merged planar store at their (partition, index) offsets.
 int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* const* locals,
                             int nlocal, int axis, const double* cut_lo, const double* cut_hi,
-                            ModelDev& merged, ScanScratch& sc, cudaStream_t st, float* wire_ms,
-                            int64_t* max_iteration) {
+                            ModelDev& merged, ScanScratch& sc, MergeScratch& ms, cudaStream_t st,
+                            float* wire_ms, int64_t* max_iteration) {
   Nccl& N = nccl();
   ncclComm_t c = (ncclComm_t)comm;
   const int P = nranks * nlocal;
   // 1. local compaction of each partition into a dense [14][cnt] buffer
   std::vector<int64_t> mine(2 * nlocal);
   std::vector<DevBuf<float>> dense(nlocal);
+  std::vector<MergeSrc> src(nlocal);
+  std::vector<int64_t> lcnt(nlocal);
   for (int j = 0; j < nlocal; ++j) {
     const ModelDev& L = *locals[j];
-    const int64_t cnt = merge_compact_dev(L.params.get(), L.cap, L.n, axis, cut_lo[j], cut_hi[j],
-                                          nullptr, 0, 0, sc, st);
+    src[j] = {L.params.get(), L.cap, L.n, cut_lo[j], cut_hi[j]};
+  }
+  merge_trim_count(src.data(), nlocal, axis, ms, sc, st, lcnt.data());
+  for (int j = 0; j < nlocal; ++j) {
+    const int64_t cnt = lcnt[j];
     dense[j].ensure((size_t)kParams * std::max<int64_t>(cnt, 1));
-    merge_compact_dev(L.params.get(), L.cap, L.n, axis, cut_lo[j], cut_hi[j], dense[j].get(),
-                      std::max<int64_t>(cnt, 1), 0, sc, st);
+    merge_trim_scatter(src[j], j, ms, dense[j].get(), std::max<int64_t>(cnt, 1), 0, st);
     mine[2 * j] = cnt;
-    mine[2 * j + 1] = L.iteration;
+    mine[2 * j + 1] = locals[j]->iteration;
   }
   // 2. (count, iteration) of every partition
   DevBuf<int64_t> meta;

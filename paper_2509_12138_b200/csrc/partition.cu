@@ -186,26 +186,39 @@ PartitionResult partition_dev(const double* host_pts, int64_t n, int nparts, dou
   return r;
 }
 
-int64_t merge_compact_dev(const float* src, int64_t spitch, int64_t n, int axis, double cut_lo,
-                          double cut_hi, float* dst, int64_t dpitch, int64_t dst_off,
-                          ScanScratch& sc, cudaStream_t st) {
-  if (n <= 0) return 0;
-  DevBuf<uint32_t> flag, pos;
-  flag.ensure(n);
-  pos.ensure(n + 1);
-  k_merge_flags<<<nb(n), 256, 0, st>>>(src, spitch, n, axis, cut_lo, cut_hi, flag.get());
-  count_launch();
-  exclusive_scan_u32(flag.get(), pos.get(), n, sc, st);
-  uint32_t cnt = 0;
-  DSG_CUDA_CHECK(cudaMemcpyAsync(&cnt, pos.get() + n, 4, cudaMemcpyDeviceToHost, st));
-  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
-  if (dst) {
-    k_merge_scatter<<<nb(n), 256, 0, st>>>(src, spitch, n, flag.get(), pos.get(), dst, dpitch,
-                                           dst_off);
-    count_launch();
-    DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+void merge_trim_count(const MergeSrc* src, int np, int axis, MergeScratch& ms, ScanScratch& sc,
+                      cudaStream_t st, int64_t* counts) {
+  ms.base.assign(np + 1, 0);
+  for (int k = 0; k < np; ++k) ms.base[k + 1] = ms.base[k] + src[k].n + 1;
+  ms.flag.ensure(std::max<int64_t>(ms.base[np], 1));
+  ms.pos.ensure(std::max<int64_t>(ms.base[np], 1));
+  ms.cnt.ensure(std::max(np, 1));
+  for (int k = 0; k < np; ++k) {
+    const MergeSrc& s = src[k];
+    uint32_t* pos = ms.pos.get() + ms.base[k];
+    if (s.n > 0) {
+      uint32_t* flag = ms.flag.get() + ms.base[k];
+      k_merge_flags<<<nb(s.n), 256, 0, st>>>(s.params, s.pitch, s.n, axis, s.cut_lo, s.cut_hi, flag);
+      count_launch();
+      exclusive_scan_u32(flag, pos, s.n, sc, st);
+      DSG_CUDA_CHECK(cudaMemcpyAsync(ms.cnt.get() + k, pos + s.n, 4, cudaMemcpyDeviceToDevice, st));
+    } else {
+      DSG_CUDA_CHECK(cudaMemsetAsync(ms.cnt.get() + k, 0, 4, st));
+    }
   }
-  return cnt;
+  std::vector<uint32_t> c(std::max(np, 1));
+  DSG_CUDA_CHECK(cudaMemcpyAsync(c.data(), ms.cnt.get(), 4ull * np, cudaMemcpyDeviceToHost, st));
+  DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  for (int k = 0; k < np; ++k) counts[k] = c[k];
+}
+
+void merge_trim_scatter(const MergeSrc& src, int k, MergeScratch& ms, float* dst, int64_t dpitch,
+                        int64_t dst_off, cudaStream_t st) {
+  if (src.n <= 0) return;
+  k_merge_scatter<<<nb(src.n), 256, 0, st>>>(src.params, src.pitch, src.n,
+                                             ms.flag.get() + ms.base[k], ms.pos.get() + ms.base[k],
+                                             dst, dpitch, dst_off);
+  count_launch();
 }
 
 }  // namespace dsg

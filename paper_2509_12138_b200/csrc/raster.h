@@ -86,9 +86,9 @@ struct Frame {
   DevBuf<float> rgb, T, dL, Tband;
   DevBuf<uint32_t> last;
   DevBuf<int32_t> ncontrib;
-  // backward partials: [n_dup][8 sub-tiles][8] (values 0..7) then [n_dup][8] (value 8)
+  // backward partials: [n_dup][kPartRows][8] (values 0..7) then [n_dup][kPartRows] (value 8)
   DevBuf<float> partials;
-  DevBuf<uint32_t> tmask;     // 8-bit touched-sub-tile mask per duplicate, 4 per word
+  DevBuf<uint32_t> tmask;     // 8-bit touched-row mask per duplicate, 4 per word
   // device copy of the blend kernels' guard-band context (read by the rare
   // fp64 path through a pointer, so it never lands on the thread stack)
   DevBuf<uint8_t> evalctx;
@@ -139,13 +139,22 @@ struct ModelDev {
   void reserve(int64_t c);
 };
 
+// Backward partial rows per (splat, tile) duplicate. With DSG_BWD_FOLD the
+// four sub-tile warps of a blend-backward CTA fold their values per list
+// entry in shared memory (fixed sub-tile order), so each duplicate has one
+// row per half tile; without it, one row per 8x4 sub-tile.
+#ifndef DSG_BWD_FOLD
+#define DSG_BWD_FOLD 0
+#endif
+constexpr int kPartRows = DSG_BWD_FOLD ? 2 : 8;
+
 struct ChainArgs {
   const float* params;
   int64_t pitch, n;
   CamDev cam;
   const uint32_t* tcount;
   const uint32_t* dup_base;
-  const float* partials;    // blend.cu layout: [n_dup][8][8] then [n_dup][8]
+  const float* partials;    // blend.cu layout: [n_dup][kPartRows][8] then [n_dup][kPartRows]
   int64_t n_dup;
   const uint32_t* tmask;
   float* grads;     // [14][pitch]
@@ -216,12 +225,25 @@ struct PartitionResult {
 };
 PartitionResult partition_dev(const double* host_pts, int64_t n, int nparts, double margin,
                               SortScratch& ss, ScanScratch& sc, cudaStream_t st);
-// merge_models keep rule (partition.hpp:120): compact splats whose mu[axis]
-// lies in [cut_lo, cut_hi) into dst (planar, pitch dpitch) at dst_off; returns
-// the survivor count (dst may be null to count only).
-int64_t merge_compact_dev(const float* src, int64_t spitch, int64_t n, int axis, double cut_lo,
-                          double cut_hi, float* dst, int64_t dpitch, int64_t dst_off,
-                          ScanScratch& sc, cudaStream_t st);
+// merge_models keep rule (partition.hpp:120): splats whose mu[axis] lies in
+// [cut_lo, cut_hi) are kept, in index order, into a planar dst at dst_off.
+// Several partitions at once: merge_trim_count flags and scans all of them
+// and reads the counts back with one synchronize; merge_trim_scatter then
+// writes partition k's survivors. The flags and prefix sums stay in `ms`
+// between the two calls (no allocation once warm).
+struct MergeScratch {
+  DevBuf<uint32_t> flag, pos, cnt;
+  std::vector<int64_t> base;
+};
+struct MergeSrc {
+  const float* params;
+  int64_t pitch, n;
+  double cut_lo, cut_hi;
+};
+void merge_trim_count(const MergeSrc* src, int np, int axis, MergeScratch& ms, ScanScratch& sc,
+                      cudaStream_t st, int64_t* counts);
+void merge_trim_scatter(const MergeSrc& src, int k, MergeScratch& ms, float* dst, int64_t dpitch,
+                        int64_t dst_off, cudaStream_t st);
 // densify_and_prune + AdamState::remap on the device (densify.cu). `spare`
 // provides the output storage and receives the old one; rng_state is the
 // persistent splitmix64 state of the run's densify Rng (advanced in place).
@@ -246,7 +268,7 @@ void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(void* comm);
 int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* const* locals,
                             int nlocal, int axis, const double* cut_lo, const double* cut_hi,
-                            ModelDev& merged, ScanScratch& sc, cudaStream_t st,
+                            ModelDev& merged, ScanScratch& sc, MergeScratch& ms, cudaStream_t st,
                             float* wire_ms = nullptr, int64_t* max_iteration = nullptr);
 void gather_bands_dev(void* comm, int nranks, int rank, float* rgb, int width, int height,
                       const std::vector<int>& row0, const std::vector<int>& row1, cudaStream_t st);

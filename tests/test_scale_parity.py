@@ -178,3 +178,44 @@ def test_config2_three_step_trajectory(ctx, ref):
     b = ref.train_partition_full(seeds, tv, cfg, shards=_os.cpu_count() or 1, loss_trace=True)
     _record("config2_trajectory", {"device": a.loss_trace.tolist(), "reference": b.loss_trace.tolist()})
     np.testing.assert_allclose(a.loss_trace, b.loss_trace, rtol=1e-4)
+
+
+def test_config5_merged_4k_render(ctx, ref, rt_cloud):
+    """Config 5's path at RT scale: the 8 partitions' seed models ghost-trimmed
+    and merged on the device (merge_models, partition.hpp:109-126), then the
+    merged 18M-splat model rendered at 3840x2160 (explicit camera, as
+    runtime.hpp:476-520 renders the merged model). Against the reference:
+    merge bit-exact (fp32-exact inputs), splat order bit-exact, image <= 1e-3,
+    contributor counts exact. (The 106.7M RM model is beyond what the CPU
+    reference renders in a test's time.)"""
+    from paper_2509_12138_b200.types import Camera
+    from host_partition import merge_models
+    pts, cols, _ = rt_cloud
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    parts = api.partition_cloud(pts, 8, 3.0 * nn, ctx=ctx)
+    models, hosts = [], []
+    for k, p in enumerate(parts):
+        idx = np.concatenate([p.owned_indices, p.ghost_indices]).astype(np.int64)
+        dm = api.seed_gaussians(np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx]), 3,
+                                ctx=ctx)
+        h = dm.download()
+        h.origin_partition = k
+        models.append(dm)
+        hosts.append(h)
+    merged = api.merge_models(models, parts, ctx=ctx).download()
+    expect = merge_models(hosts, parts)
+    np.testing.assert_array_equal(merged.params, expect.params)
+    del models
+    c = (pts.min(0) + pts.max(0)) * 0.5
+    rig = scenes.rig_for_cloud(pts, 28, 16, 1024)
+    cam = Camera(rig[0].position, tuple(float(v) for v in c), (0.0, 1.0, 0.0), 0.9, 3840, 2160,
+                 rig[0].near, rig[0].far)
+    a = api.render(merged, cam, RenderConfig(), ctx=ctx)
+    b = ref.render(merged, cam, RenderConfig())
+    rep = {"merged": int(len(merged)), "splat_order_bit_exact": bool(np.array_equal(a.splat_order, b.splat_order)),
+           "img_max_abs": float(np.max(np.abs(a.color - b.color))),
+           "ncontrib_mismatch_px": int(np.sum(a.per_pixel_contributor_count != b.per_pixel_contributor_count))}
+    _record("config5_rt_merged_4k", rep)
+    assert rep["splat_order_bit_exact"], rep
+    assert rep["img_max_abs"] <= 1e-3, rep
+    assert rep["ncontrib_mismatch_px"] == 0, rep
