@@ -60,15 +60,15 @@ __global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
   bool touched = false;
   const uint32_t cnt = a.tcount[i];
   if (cnt) {
-    // fold (duplicate, row) slots in fixed tile-then-row order
+    // fold (duplicate, sub-tile) slots in fixed tile-then-sub-tile order
     const uint32_t base = a.dup_base[i];
     for (uint32_t k = 0; k < cnt; ++k) {
       const uint32_t d = base + k;
       uint32_t m = (a.tmask[d >> 2] >> (8 * (d & 3))) & 0xffu;
       if (!m) continue;
       touched = true;
-      const float4* pp = reinterpret_cast<const float4*>(a.partials) + (size_t)d * kPartRows * 2;
-      const float* p8 = a.partials + (size_t)a.n_dup * kPartRows * 8 + (size_t)d * kPartRows;
+      const float4* pp = reinterpret_cast<const float4*>(a.partials) + (size_t)d * 8 * 2;
+      const float* p8 = a.partials + (size_t)a.n_dup * 64 + (size_t)d * 8;
       while (m) {
         const int w = __ffs(m) - 1;
         m &= m - 1;

@@ -86,9 +86,9 @@ struct Frame {
   DevBuf<float> rgb, T, dL, Tband;
   DevBuf<uint32_t> last;
   DevBuf<int32_t> ncontrib;
-  // backward partials: [n_dup][kPartRows][8] (values 0..7) then [n_dup][kPartRows] (value 8)
+  // backward partials: [n_dup][8 sub-tiles][8] (values 0..7) then [n_dup][8] (value 8)
   DevBuf<float> partials;
-  DevBuf<uint32_t> tmask;     // 8-bit touched-row mask per duplicate, 4 per word
+  DevBuf<uint32_t> tmask;     // 8-bit touched-sub-tile mask per duplicate, 4 per word
   // device copy of the blend kernels' guard-band context (read by the rare
   // fp64 path through a pointer, so it never lands on the thread stack)
   DevBuf<uint8_t> evalctx;
@@ -139,22 +139,13 @@ struct ModelDev {
   void reserve(int64_t c);
 };
 
-// Backward partial rows per (splat, tile) duplicate. With DSG_BWD_FOLD the
-// four sub-tile warps of a blend-backward CTA fold their values per list
-// entry in shared memory (fixed sub-tile order), so each duplicate has one
-// row per half tile; without it, one row per 8x4 sub-tile.
-#ifndef DSG_BWD_FOLD
-#define DSG_BWD_FOLD 0
-#endif
-constexpr int kPartRows = DSG_BWD_FOLD ? 2 : 8;
-
 struct ChainArgs {
   const float* params;
   int64_t pitch, n;
   CamDev cam;
   const uint32_t* tcount;
   const uint32_t* dup_base;
-  const float* partials;    // blend.cu layout: [n_dup][kPartRows][8] then [n_dup][kPartRows]
+  const float* partials;    // blend.cu layout: [n_dup][8][8] then [n_dup][8]
   int64_t n_dup;
   const uint32_t* tmask;
   float* grads;     // [14][pitch]
