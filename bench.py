@@ -255,7 +255,10 @@ def train_config(args, rank: int, iterations: int) -> TrainConfig:
 KERNEL_OF_STAGE = {"preprocess": "k_preprocess", "depth_sort": "k_onesweep (depth)",
                    "scan_duplicate": "k_duplicate", "tile_sort_ranges": "k_onesweep (tile)",
                    "blend_fwd": "k_blend_fwd<0>", "loss": "k_ssim_stats+k_loss_grad",
-                   "blend_bwd": "k_blend_bwd", "chain": "k_chain", "adam": "k_adam"}
+                   "blend_bwd": "k_blend_bwd", "chain": "k_chain", "adam": "k_adam",
+                   "chain_adam": "k_chain<true>"}
+# dsg_train fuses the chain and Adam into one kernel unless DSG_FUSE_ADAM=0
+FUSED_ADAM = os.environ.get("DSG_FUSE_ADAM", "1") != "0"
 
 
 def algorithmic_bytes(stage: str, n: int, nv: int, npix: int, n_dup: int) -> float:
@@ -270,6 +273,8 @@ def algorithmic_bytes(stage: str, n: int, nv: int, npix: int, n_dup: int) -> flo
         "blend_bwd": 5.0 * n_dup + 68.0 * n_dup + 20.0 * npix + 36.0 * n_dup,  # + >=1 partial/entry
         "chain": 112.0 * n + 36.0 * n_dup + 4.0 * n_dup,   # params+grads, partials, masks
         "adam": 412.0 * n,                                  # §8d 392 B/G + 20 B/G fused stats
+        # fused: params r+w, moments r+w, stats r+w, counts/slots, partials, masks
+        "chain_adam": 112.0 * n + 224.0 * n + 24.0 * n + 8.0 * n + 36.0 * n_dup + 4.0 * n_dup,
     }[stage]
 
 
@@ -565,6 +570,8 @@ def run_ours(args, dist: Dist):
     prof_total, stages = ctx.last_timing()
     ctx.set_profiling(False)
     stage_ms = {s: float(v) / pk for s, v in zip(api.STAGES, stages)}
+    if FUSED_ADAM:  # one launch does chain + Adam; the "adam" mark holds only the densify check
+        stage_ms["chain_adam"] = stage_ms.pop("chain") + stage_ms.pop("adam")
     fs = api.frame_stats(ctx)
     n_dup, nv_vis = fs["n_dup"], fs["n_visible"]
     work = api.frame_work(ctx)  # composited pairs C and fp64 termination fix-ups, last view

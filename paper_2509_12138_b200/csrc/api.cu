@@ -1236,6 +1236,11 @@ int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
     if (cfg->iterations == 0) return;
     const int64_t iters = cfg->iterations;
     const int64_t until = (int64_t)(cfg->densify_stop_fraction * (double)iters);
+    // DSG_FUSE_ADAM=0: separate chain and Adam launches (A/B; same bits)
+    static const bool fuse_adam = [] {
+      const char* e = std::getenv("DSG_FUSE_ADAM");
+      return !(e && e[0] == '0');
+    }();
     // Rng densify_rng(seed ^ 0xd3a51f11) (trainer.hpp:165): splitmix64 state
     // after the constructor's two warm-up draws (rng.hpp:25-30)
     uint64_t drng = (cfg->seed ^ 0xd3a51f11ULL) ^ 0x853c49e6748fea9bULL;
@@ -1345,6 +1350,9 @@ int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
       if (views->host)  // view slot free for the upload two steps ahead
         DSG_CUDA_CHECK(cudaEventRecord(ctx->ev_consumed[slot], st));
       tm.mark(6, st);
+      const double decay = std::pow(cfg->lr_mu_decay, (double)it / (double)iters);
+      const double rates[5] = {cfg->lr_mu * decay, cfg->lr_scale, cfg->lr_rot, cfg->lr_opacity,
+                               cfg->lr_color};
       if (!empty) blend_backward(f, m.params.get(), m.cap, cam, rd, st);
       tm.mark(7, st);
       if (empty) {
@@ -1365,14 +1373,18 @@ int dsg_train_checkpointed(dsg_ctx ctx, dsg_model model, dsg_views views,
         a.grads = m.grads.get();
         a.dmean = m.dmean.get();
         a.touch = m.touch.get();
-        chain_3d(a, st);
+        if (fuse_adam) {
+          m.adam_step += 1;  // chain + Adam in one pass (no gradient store)
+          chain_adam(a, make_adam(m, rates, cfg->adam, m.adam_step, true), st);
+        } else {
+          chain_3d(a, st);
+        }
       }
       tm.mark(8, st);
-      const double decay = std::pow(cfg->lr_mu_decay, (double)it / (double)iters);
-      const double rates[5] = {cfg->lr_mu * decay, cfg->lr_scale, cfg->lr_rot, cfg->lr_opacity,
-                               cfg->lr_color};
-      m.adam_step += 1;
-      adam_update(make_adam(m, rates, cfg->adam, m.adam_step, true), st);
+      if (empty || !fuse_adam) {
+        m.adam_step += 1;
+        adam_update(make_adam(m, rates, cfg->adam, m.adam_step, true), st);
+      }
       m.iteration += 1;
       // densify at (it+1) % interval == 0 while (it+1) < stop (trainer.hpp:195-202)
       if (cfg->densify_interval > 0 && (it + 1) % cfg->densify_interval == 0 && (it + 1) < until)

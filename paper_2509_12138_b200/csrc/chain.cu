@@ -11,6 +11,7 @@
 // isotropic identity-rotation splats exactly 0 in either precision.
 #include "dsg_internal.h"
 #include "raster.h"
+#include "adam_math.cuh"
 
 #ifndef DSG_CHAIN_REAL
 #define DSG_CHAIN_REAL float
@@ -52,7 +53,15 @@ __device__ __forceinline__ void mm3(const Real* a, const Real* b, Real* r) {
 #ifndef DSG_CHAIN_MINB
 #define DSG_CHAIN_MINB 4  // 4 CTAs/SM (64 regs, 72 B spill): 0.34 vs 0.49 ms unbounded
 #endif
-__global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
+#ifndef DSG_CHAIN_PAIRS
+#define DSG_CHAIN_PAIRS 0
+#endif
+
+// kAdam: the training step's fused form — the splat's gradients go straight
+// from registers into the Adam update (adam_math.cuh) instead of through the
+// planar gradient store (saves 56 B written + 124 B read per splat).
+template <bool kAdam>
+__global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a, AdamArgs ad) {
   DSG_PDL_ENTRY();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.n) return;
@@ -69,6 +78,46 @@ __global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
       touched = true;
       const float4* pp = reinterpret_cast<const float4*>(a.partials) + (size_t)d * 8 * 2;
       const float* p8 = a.partials + (size_t)a.n_dup * 64 + (size_t)d * 8;
+#if DSG_CHAIN_PAIRS
+      // two rows per round trip (both loads issued before either is summed;
+      // the sums stay in sub-tile order)
+      while (m) {
+        const int w = __ffs(m) - 1;
+        m &= m - 1;
+        const bool two = m != 0;
+        const int w2 = two ? __ffs(m) - 1 : w;
+        if (two) m &= m - 1;
+        const float4 q0 = __ldg(pp + 2 * w), q1 = __ldg(pp + 2 * w + 1);
+        const float e8 = __ldg(p8 + w);
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+        float f8 = 0.f;
+        if (two) {
+          r0 = __ldg(pp + 2 * w2);
+          r1 = __ldg(pp + 2 * w2 + 1);
+          f8 = __ldg(p8 + w2);
+        }
+        acc[0] += q0.x;
+        acc[1] += q0.y;
+        acc[2] += q0.z;
+        acc[3] += q0.w;
+        acc[4] += q1.x;
+        acc[5] += q1.y;
+        acc[6] += q1.z;
+        acc[7] += q1.w;
+        acc[8] += e8;
+        if (two) {
+          acc[0] += r0.x;
+          acc[1] += r0.y;
+          acc[2] += r0.z;
+          acc[3] += r0.w;
+          acc[4] += r1.x;
+          acc[5] += r1.y;
+          acc[6] += r1.z;
+          acc[7] += r1.w;
+          acc[8] += f8;
+        }
+      }
+#else
       while (m) {
         const int w = __ffs(m) - 1;
         m &= m - 1;
@@ -83,16 +132,21 @@ __global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
         acc[7] += q1.w;
         acc[8] += p8[w];
       }
+#endif
     }
   }
   float* G = a.grads;
   const int64_t P = a.pitch;
   if (!touched) {
+    if constexpr (kAdam) {
+      adam_splat(ad, i, [](int) { return 0.f; }, false, 0.f, 0.f);
+    } else {
 #pragma unroll
-    for (int k = 0; k < kParams; ++k) G[k * P + i] = 0.f;
-    a.dmean[i] = 0.f;
-    a.dmean[P + i] = 0.f;
-    a.touch[i] = 0;
+      for (int k = 0; k < kParams; ++k) G[k * P + i] = 0.f;
+      a.dmean[i] = 0.f;
+      a.dmean[P + i] = 0.f;
+      a.touch[i] = 0;
+    }
     return;
   }
   Real p[kParams];
@@ -226,28 +280,42 @@ __global__ void __launch_bounds__(256, DSG_CHAIN_MINB) k_chain(ChainArgs a) {
     gqn[k] = v;
   }
   Real dot = gqn[0] * qn[0] + gqn[1] * qn[1] + gqn[2] * qn[2] + gqn[3] * qn[3];
-  G[0 * P + i] = (float)gmu0;
-  G[1 * P + i] = (float)gmu1;
-  G[2 * P + i] = (float)gmu2;
-  G[3 * P + i] = (float)gls[0];
-  G[4 * P + i] = (float)gls[1];
-  G[5 * P + i] = (float)gls[2];
+  float g[kParams];
+  g[0] = (float)gmu0;
+  g[1] = (float)gmu1;
+  g[2] = (float)gmu2;
+  g[3] = (float)gls[0];
+  g[4] = (float)gls[1];
+  g[5] = (float)gls[2];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) G[(6 + k) * P + i] = (float)((gqn[k] - dot * qn[k]) / qnorm);
-  G[10 * P + i] = (float)(acc[8] * op * (Real(1.0) - op));
-  G[11 * P + i] = (float)acc[5];
-  G[12 * P + i] = (float)acc[6];
-  G[13 * P + i] = (float)acc[7];
-  a.dmean[i] = (float)gmx;
-  a.dmean[P + i] = (float)gmy;
-  a.touch[i] = 1;
+  for (int k = 0; k < 4; ++k) g[6 + k] = (float)((gqn[k] - dot * qn[k]) / qnorm);
+  g[10] = (float)(acc[8] * op * (Real(1.0) - op));
+  g[11] = (float)acc[5];
+  g[12] = (float)acc[6];
+  g[13] = (float)acc[7];
+  if constexpr (kAdam) {
+    adam_splat(ad, i, [&](int k) { return g[k]; }, true, (float)gmx, (float)gmy);
+  } else {
+#pragma unroll
+    for (int k = 0; k < kParams; ++k) G[k * P + i] = g[k];
+    a.dmean[i] = (float)gmx;
+    a.dmean[P + i] = (float)gmy;
+    a.touch[i] = 1;
+  }
 }
 
 }  // namespace
 
 void chain_3d(const ChainArgs& a, cudaStream_t st) {
   if (a.n == 0) return;
-  pdl_launch(k_chain, (unsigned)((a.n + 255) / 256), 256, 0, st, a);
+  pdl_launch(k_chain<false>, (unsigned)((a.n + 255) / 256), 256, 0, st, a, AdamArgs{});
+  count_launch();
+  DSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void chain_adam(const ChainArgs& a, const AdamArgs& ad, cudaStream_t st) {
+  if (a.n == 0) return;
+  pdl_launch(k_chain<true>, (unsigned)((a.n + 255) / 256), 256, 0, st, a, ad);
   count_launch();
   DSG_CUDA_CHECK(cudaGetLastError());
 }

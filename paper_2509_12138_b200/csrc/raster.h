@@ -194,6 +194,9 @@ void blend_backward(Frame& f, const float* params, int64_t pitch, const CamDev& 
                     const RenderDev& rd, cudaStream_t st);
 void chain_3d(const ChainArgs& a, cudaStream_t st);
 void adam_update(const AdamArgs& a, cudaStream_t st);
+// K7 + K9 in one launch (the training step): gradients never reach HBM;
+// a.grads / dmean / touch are not written.
+void chain_adam(const ChainArgs& a, const AdamArgs& ad, cudaStream_t st);
 // Masked L1 + D-SSIM on f.rgb vs (gt, mask); writes f.dL and the loss into
 // `out` (default f.loss_out[0]; device). gt planar fp32 [3][h*w], mask u8 [h*w].
 // K11: stamp render_mask discs of `radius` px into a zeroed byte mask.

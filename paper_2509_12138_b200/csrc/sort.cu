@@ -174,7 +174,8 @@ __global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
   }
   __syncthreads();
 
-  // Thread d owns digit d: exclusive offsets across warps, block total.
+  // Thread d owns digit d: exclusive offsets across warps, block total,
+  // published at once so later partitions can sum past this one.
   const int d = tid;
   uint32_t total = 0;
 #pragma unroll
@@ -183,13 +184,30 @@ __global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
     sm.warp_hist[w][d] = total;
     total += c;
   }
-  // Decoupled look-back over earlier partitions for this digit.
   volatile uint32_t* vs = status;
+  vs[(size_t)part * kRadix + d] = (part == 0 ? kFlagPrefix : kFlagAgg) | total;
+  uint32_t bagg;
+  uint32_t bex = block_exclusive_sum<kSortThreads>(total, &bagg, sm.scan);
+  sm.block_excl[d] = bex;
+  __syncthreads();
+
+  // Stage the partition digit-sorted in shared memory: only block-local
+  // offsets are needed, so this happens before the look-back, which then
+  // runs with the key registers dead (a wider window without spills) and
+  // gives the predecessors more time to publish their prefixes.
+#pragma unroll
+  for (int i = 0; i < kSortItems; ++i) {
+    uint32_t dg = dig[i];
+    if (dg < kRadix) {
+      uint32_t pos = sm.block_excl[dg] + sm.warp_hist[warp][dg] + rank[i];
+      sm.keys[pos] = k[i];
+      sm.vals[pos] = v[i];
+    }
+  }
+
+  // Decoupled look-back over earlier partitions for this digit.
   uint32_t excl = 0;
-  if (part == 0) {
-    vs[d] = kFlagPrefix | total;
-  } else {
-    vs[(size_t)part * kRadix + d] = kFlagAgg | total;
+  if (part != 0) {
     int64_t p = (int64_t)part - 1;
     // read kLookback predecessors per round trip (partition 0 always holds a
     // prefix): the first wave of resident partitions otherwise walks back
@@ -219,20 +237,6 @@ __global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
     vs[(size_t)part * kRadix + d] = kFlagPrefix | (excl + total);
   }
   sm.global_base[d] = gscan[d] + excl;
-  uint32_t bagg;
-  uint32_t bex = block_exclusive_sum<kSortThreads>(total, &bagg, sm.scan);
-  sm.block_excl[d] = bex;
-  __syncthreads();
-
-#pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    uint32_t dg = dig[i];
-    if (dg < kRadix) {
-      uint32_t pos = sm.block_excl[dg] + sm.warp_hist[warp][dg] + rank[i];
-      sm.keys[pos] = k[i];
-      sm.vals[pos] = v[i];
-    }
-  }
   __syncthreads();
   const int64_t remain = n - base;
   const int count = remain < kPart ? (int)remain : kPart;

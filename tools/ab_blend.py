@@ -37,6 +37,16 @@ def run(out, n, res, views, oracle_view=None):
         res_[f"loss{k}"] = np.array([lo.loss])
         res_[f"grads{k}"] = gb.grads.astype(np.float32)
         res_[f"touch{k}"] = gb.touch_count
+    # a short training run on the same views (dsg_train: fused chain + Adam,
+    # densification inside), then the trained parameters, moments and stats
+    from paper_2509_12138_b200.types import TrainConfig
+    dv = api.DeviceViews.synthesize(ctx, gt, rcfg, cams, pts, True, 2.0, 2.0)
+    cfg = TrainConfig(iterations=2 * views, seed=1, densify_interval=3)
+    fl, trace = api.train_device(seeds, dv, cfg, loss_trace=True)
+    res_["train_params"] = seeds.download().params.astype(np.float32)
+    m, v, st = seeds.adam_state()
+    res_["train_m"], res_["train_v"] = m.astype(np.float32), v.astype(np.float32)
+    res_["train_trace"] = trace
     if oracle_view is not None:
         # oracle contributor counts of one view (CPU, fp64 reference order)
         from oracle import Oracle
