@@ -256,7 +256,7 @@ KERNEL_OF_STAGE = {"preprocess": "k_preprocess", "depth_sort": "k_onesweep (dept
                    "scan_duplicate": "k_duplicate", "tile_sort_ranges": "k_onesweep (tile)",
                    "blend_fwd": "k_blend_fwd<0>", "loss": "k_ssim_stats+k_loss_grad",
                    "blend_bwd": "k_blend_bwd", "chain": "k_chain", "adam": "k_adam",
-                   "chain_adam": "k_chain<true>"}
+                   "chain_adam": "k_chain<1>"}
 # dsg_train fuses the chain and Adam into one kernel unless DSG_FUSE_ADAM=0
 FUSED_ADAM = os.environ.get("DSG_FUSE_ADAM", "1") != "0"
 
