@@ -390,3 +390,46 @@ def test_frame_work_counts_composited_pairs(ctx):
     w = api.frame_work(ctx)
     assert w["composited"] == int(np.sum(r.per_pixel_contributor_count)) > 0
     assert 0 <= w["term_changed"] <= w["term_fixups"]
+
+
+FUSE_SCRIPT = r"""
+import os, sys, numpy as np
+sys.path.insert(0, os.environ["ROOT"])
+from paper_2509_12138_b200 import api, scenes
+from paper_2509_12138_b200.types import RenderConfig, TrainConfig
+ctx = api.Context(0)
+pts, cols, _ = scenes.kingsnake(30000, seed=2)
+nn = api.median_nn_spacing(pts, ctx=ctx)
+rig = scenes.rig_for_cloud(pts, 8, 4, 128)
+gt = api.ground_truth_model(pts, cols, nn, 0.97, ctx=ctx)
+views = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), rig[:6], pts, True, 2.0, 2.0)
+dm = api.seed_gaussians(pts, cols, 3, ctx=ctx)
+cfg = TrainConfig(iterations=16, seed=3, densify_interval=4, densify_grad_threshold=1e-5)
+fl, trace = api.train_device(dm, views, cfg, loss_trace=True)
+m, v, st = dm.adam_state()
+np.savez(sys.argv[1], params=dm.download().params, m=m, v=v, trace=trace, step=np.array([st]))
+"""
+
+
+def test_fused_chain_adam_bit_identical(tmp_path):
+    """dsg_train's fused chain + Adam kernel (gradients never stored) against
+    the separate k_chain and k_adam launches (DSG_FUSE_ADAM=0): parameters,
+    moments and loss trace bit-identical over 16 steps with densification."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "fuse.py"
+    script.write_text(FUSE_SCRIPT)
+    out = {}
+    for flag in ("0", "1"):
+        path = str(tmp_path / f"fuse{flag}.npz")
+        env = dict(os.environ, ROOT=root, DSG_FUSE_ADAM=flag)
+        r = subprocess.run([sys.executable, str(script), path], capture_output=True, text=True,
+                           timeout=300, env=env)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        out[flag] = np.load(path)
+    a, b = out["0"], out["1"]
+    assert a["params"].shape == b["params"].shape
+    for k in ("params", "m", "v", "trace", "step"):
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)

@@ -1,5 +1,6 @@
 """Summarise an ncu --metrics gpu__time_duration.sum CSV launch list over the
-last K training steps (delimited by k_adam launches)."""
+last K training steps (each step ends with its chain launch: k_chain<1>, the
+fused chain + Adam, or k_adam after k_chain when DSG_FUSE_ADAM=0)."""
 import collections
 import csv
 import re
@@ -18,7 +19,8 @@ def main(path, steps):
         v = float(r[vi].replace(",", ""))
         ms = v / 1e6 if r[ui] == "ns" else (v / 1e3 if r[ui] in ("us", "usecond") else v)
         seq.append((re.sub(r".*::", "", re.sub(r"\(.*", "", r[ki])), ms))
-    adam = [i for i, (n, _) in enumerate(seq) if n == "k_adam"]
+    ends = [i for i, (n, _) in enumerate(seq) if n in ("k_adam", "k_chain<1>")]
+    adam = ends
     win = seq[adam[-steps - 1] + 1:] if len(adam) > steps else seq
     tot, cnt = collections.defaultdict(float), collections.Counter()
     for n, ms in win:
