@@ -194,8 +194,9 @@ def global_phase(args, dist: Dist, ctx, inp, trained, reps: int = 3):
         merged, n_merged, merge_ms = api.merge_allgather(comm, trained, inp["partition"])
     else:
         merged = api.merge_models([trained], [inp["partition"]], ctx=ctx)  # allocates
+        ctx.synchronize()
         t0 = time.perf_counter()
-        merged = api.merge_models([trained], [inp["partition"]], ctx=ctx)
+        merged = api.merge_models([trained], [inp["partition"]], ctx=ctx, out=merged)
         merge_ms = (time.perf_counter() - t0) * 1e3
         n_merged = merged.info()[0]
     c0 = inp["rig"][0]
