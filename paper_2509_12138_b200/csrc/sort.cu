@@ -124,11 +124,40 @@ struct OnesweepSmem {
   uint32_t warp_hist[kSortWarps][kRadix];
   uint32_t block_excl[kRadix];
   uint32_t global_base[kRadix];
-  K keys[kPart];
+  K keys[kPart];       // the partition as loaded (TMA), then digit-sorted for the store
   uint32_t vals[kPart];
+  uint64_t bar;        // mbarrier of the bulk loads
   uint32_t part;
   uint32_t scan[33];
 };
+
+#ifndef DSG_SORT_TMA
+#define DSG_SORT_TMA 1
+#endif
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// 1-D bulk copy global -> shared (TMA engine), completion counted in bytes
+// on an mbarrier; dst, src and bytes 16 B aligned.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
 
 template <class K>
 #ifndef DSG_SORT_MINB
@@ -142,24 +171,67 @@ __global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
   extern __shared__ __align__(16) unsigned char smem_raw[];
   OnesweepSmem<K>& sm = *reinterpret_cast<OnesweepSmem<K>*>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#if DSG_SORT_TMA
+  // The partition's keys and values arrive by two bulk copies (TMA) into the
+  // staging arrays the digit-sorted store uses later; one thread issues
+  // them as soon as the ticket is drawn, the rest zero the histograms.
+  const bool tma = ((reinterpret_cast<uintptr_t>(kin) | reinterpret_cast<uintptr_t>(vin)) & 15) == 0;
+  if (tid == 0) {
+    const uint32_t part0 = atomicAdd(counter, 1u);
+    sm.part = part0;
+    if (tma) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&sm.bar)) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      const int64_t b0 = (int64_t)part0 * kPart;
+      const int64_t c0 = n - b0 < kPart ? n - b0 : (int64_t)kPart;
+      const uint32_t kb = (uint32_t)(c0 * sizeof(K)) & ~15u, vb = (uint32_t)(c0 * 4) & ~15u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&sm.bar)),
+                   "r"(kb + vb)
+                   : "memory");
+      if (kb) bulk_load(sm.keys, kin + b0, kb, &sm.bar);
+      if (vb) bulk_load(sm.vals, vin + b0, vb, &sm.bar);
+    }
+  }
+#else
+  const bool tma = false;
   if (tid == 0) sm.part = atomicAdd(counter, 1u);
+#endif
   for (int i = tid; i < kSortWarps * kRadix; i += kSortThreads) (&sm.warp_hist[0][0])[i] = 0;
   __syncthreads();
   const uint32_t part = sm.part;
   const int64_t base = (int64_t)part * kPart;
+  const int count = n - base < kPart ? (int)(n - base) : kPart;
 
   K k[kSortItems];
   uint32_t v[kSortItems];
   uint32_t dig[kSortItems];
   uint32_t rank[kSortItems];
-  const int64_t wbase = base + (int64_t)warp * 32 * kSortItems;
+  const int wloc = warp * 32 * kSortItems;
+  if (tma) {
+    // the tail past the last whole 16 B of a short final partition
+    const int kt = (int)(((uint32_t)(count * sizeof(K)) & ~15u) / sizeof(K));
+    const int vt = (int)(((uint32_t)(count * 4) & ~15u) / 4);
+    for (int j = kt + tid; j < count; j += kSortThreads) sm.keys[j] = kin[base + j];
+    for (int j = vt + tid; j < count; j += kSortThreads) sm.vals[j] = vin[base + j];
+    mbar_wait(&sm.bar, 0);
+    __syncthreads();
 #pragma unroll
-  for (int i = 0; i < kSortItems; ++i) {
-    int64_t idx = wbase + i * 32 + lane;
-    bool valid = idx < n;
-    k[i] = valid ? kin[idx] : K(0);
-    v[i] = valid ? vin[idx] : 0u;
-    dig[i] = valid ? (uint32_t)((k[i] >> shift) & (kRadix - 1)) : 0x100u;
+    for (int i = 0; i < kSortItems; ++i) {
+      const int j = wloc + i * 32 + lane;
+      const bool valid = j < count;
+      k[i] = valid ? sm.keys[j] : K(0);
+      v[i] = valid ? sm.vals[j] : 0u;
+      dig[i] = valid ? (uint32_t)((k[i] >> shift) & (kRadix - 1)) : 0x100u;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < kSortItems; ++i) {
+      const int j = wloc + i * 32 + lane;
+      const bool valid = j < count;
+      k[i] = valid ? kin[base + j] : K(0);
+      v[i] = valid ? vin[base + j] : 0u;
+      dig[i] = valid ? (uint32_t)((k[i] >> shift) & (kRadix - 1)) : 0x100u;
+    }
   }
   const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -238,8 +310,6 @@ __global__ void __launch_bounds__(kSortThreads, DSG_SORT_MINB) k_onesweep(
   }
   sm.global_base[d] = gscan[d] + excl;
   __syncthreads();
-  const int64_t remain = n - base;
-  const int count = remain < kPart ? (int)remain : kPart;
   for (int j = tid; j < count; j += kSortThreads) {
     K key = sm.keys[j];
     uint32_t dg = (uint32_t)((key >> shift) & (kRadix - 1));
