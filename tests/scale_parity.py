@@ -157,16 +157,54 @@ def step_parity(ctx, ref, model: SplatModel, view, tcfg: TrainConfig = None, sha
         gk = api.backward(model, cam, rcfg, a, kink.astype(np.float64), ctx=ctx)
         affected = np.any(gk.grads != 0.0, axis=1)
     rep["l1_kink_pixel_channels"] = int(kink.sum())
+    dld, dlr = np.asarray(la.dL_dpixels), np.asarray(lb.dL_dpixels)
+    off = ~kink if kink.ndim == dld.ndim else np.ones_like(dld, bool)
+    rep["dL_max_rel_off_kinks"] = float(np.max(np.abs(dld - dlr)[off])
+                                        / max(float(np.max(np.abs(dlr))), 1e-300)) if off.any() else 0.0
     rep["train_step_kink_splats_excluded"] = int(affected.sum())
+    # Loss-conditioned components: each side's step starts from its own dL
+    # (fp32 device loss on its image vs fp64 reference loss on its image;
+    # the images differ by ~1e-6). The backward itself was checked above
+    # with one dL, so the device gradient from its own dL (what dsg_train
+    # uses) differs from the reference's only through that dL difference.
+    # Where that moves a gradient beyond the gradient tolerance — components
+    # that are near-total cancellations of many pixel terms — the Adam step
+    # (lr * g / (|g| + 1e-15)) inherits it; those are excluded and counted.
+    g_own = api.backward(model, cam, rcfg, a, la.dL_dpixels, ctx=ctx).grads
+    loss_cond = np.zeros_like(g_own, bool)
+    for sl in GROUPS.values():
+        x, y = g_own[:, sl], gb.grads[:, sl]
+        scale = float(np.max(np.abs(y))) if y.size else 0.0
+        loss_cond[:, sl] = (np.abs(x - y) > GRAD_RTOL * np.maximum(np.abs(x), np.abs(y))
+                            + GRAD_FLOOR * scale)
+    rep["train_step_loss_conditioned_excluded"] = int(loss_cond.sum())
+    # Step 1 of Adam maps a gradient g to lr * g / (|g| + eps) (eps = 1e-15),
+    # whose slope lr * eps / (|g| + eps)^2 turns the gradient tolerance into
+    # a step tolerance: with tol_g the tolerance at the reference gradient
+    # and m = |g| - tol_g > 0 the smallest magnitude it admits, the step may
+    # move by up to lr * eps * tol_g / m^2. Components with m <= 0 are below
+    # the floor (their sign is not pinned by the gradient tolerance).
+    eps = float(tcfg.adam.epsilon)
     flips, strong_bad = 0, 0
     for sl in GROUPS.values():
         gs = np.abs(gb.grads[:, sl])
-        strong = gs >= GRAD_FLOOR * gs.max() if gs.max() > 0 else np.zeros_like(gs, bool)
+        tol_g = GRAD_RTOL * gs + GRAD_FLOOR * gs.max()
+        margin = gs - tol_g
+        strong = (gs >= GRAD_FLOOR * gs.max()) & (margin > 0) if gs.max() > 0 \
+            else np.zeros_like(gs, bool)
         strong &= ~affected[:, None]
+        strong &= ~loss_cond[:, sl]
         x, y = da[:, sl], db[:, sl]
-        bad = np.abs(x - y) > ADAM_RTOL * np.abs(y) + 1e-6 * max(float(np.abs(y).max()), 1e-30)
+        eps_term = np.abs(y) * eps * tol_g / np.maximum(margin, 1e-300) ** 2
+        bad = (np.abs(x - y) > ADAM_RTOL * np.abs(y) + 1e-6 * max(float(np.abs(y).max()), 1e-30)
+               + np.where(strong, eps_term, 0.0))
         strong_bad += int((bad & strong).sum())
         flips += int((bad & ~strong).sum())
+        for i, c in np.argwhere(bad & strong)[:8]:  # diagnostics
+            rep.setdefault("train_step_bad", []).append(
+                [int(i), int(sl.start + c), float(x[i, c]), float(y[i, c]),
+                 float(ga.grads[i, sl.start + c]), float(gb.grads[i, sl.start + c]),
+                 float(gs[i, c] / gs.max())])
     rep["train_step_loss_rel"] = abs(ta.final_loss - tb.final_loss) / max(abs(tb.final_loss), 1e-300)
     rep["train_step_bad_above_floor"] = strong_bad
     rep["train_step_sign_flips_below_floor"] = flips

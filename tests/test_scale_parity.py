@@ -1,4 +1,4 @@
-"""Parity at the benched and named configurations (BASELINE configs 1-3).
+"""Parity at the benched and named configurations (BASELINE configs 1-5).
 
 Every check in tests/scale_parity.py (splat order and per-tile lists
 bit-exact, image <= 1e-3, gradients <= 1e-4 relative with the per-group
@@ -11,6 +11,9 @@ floor, touch counts exact, Adam, one full train iteration) runs on:
     owned / ghost lists and cuts bit-exact against partition_cloud
     (partition.hpp:42-104), the partition's background mask bit-exact
     (render.hpp:210-233), and the step checks on its seeds
+  * config 4: the 106.7M RM cloud in 8 slabs (every partition bit-exact)
+    and one 13.4M-splat partition's step at 2048^2
+  * config 5: the RT partitions' merge and the merged model's 4K render
 
 Inputs are built the way bench.py builds them (device kNN seeds and
 median NN spacing, device-synthesized GT views); the device values are
@@ -72,6 +75,11 @@ def _assert_pass(rep):
     assert rep["touch_count_exact"], rep
     assert rep["adam_worst_over_tol"] <= 1.0, rep
     assert rep["train_step_bad_above_floor"] == 0, rep
+    # the loss-conditioned exclusion stays a small fraction of the step, and
+    # the two dL images agree away from the L1 kinks
+    assert rep["train_step_loss_conditioned_excluded"] <= 1e-3 * rep["train_step_scalars"], rep
+    # (the SSIM gradient amplifies the ~1e-6 image difference by ~1/C2)
+    assert rep["dL_max_rel_off_kinks"] <= 1e-3, rep
     assert rep["loss_rel"] <= 1e-4, rep
     # contributor counts: exact (termination near the floor is re-decided in fp64)
     assert rep["ncontrib_mismatch_px"] == 0, rep
@@ -219,3 +227,44 @@ def test_config5_merged_4k_render(ctx, ref, rt_cloud):
     assert rep["splat_order_bit_exact"], rep
     assert rep["img_max_abs"] <= 1e-3, rep
     assert rep["ncontrib_mismatch_px"] == 0, rep
+
+
+def test_config4_rm_partition_and_step(ctx, ref):
+    """Config 4's shape: the 106.7M-point RM cloud (device generator) in 8
+    slabs — owned / ghost lists and cuts of every partition bit-exact against
+    partition_cloud — then one partition's mask, GT view and seeds at 2048^2
+    and the full step check (lists, order, image, n_contrib, gradients, Adam,
+    one train iteration) against the reference on its 13.4M splats."""
+    pts, cols, _ = scenes.make_cloud("rm", scenes.SIZES["rm"], seed=1, ctx=ctx)
+    nn = api.median_nn_spacing(pts, ctx=ctx)
+    margin = 3.0 * nn
+    a = api.partition_cloud(pts, 8, margin, ctx=ctx)
+    b = ref.partition_cloud(pts, 8, margin)
+    summary = []
+    for pa, pb in zip(a, b):
+        assert pa.cut_axis == pb.cut_axis
+        assert pa.cut_lo == pb.cut_lo and pa.cut_hi == pb.cut_hi
+        np.testing.assert_array_equal(pa.owned_indices, pb.owned_indices)
+        np.testing.assert_array_equal(pa.ghost_indices, pb.ghost_indices)
+        summary.append([int(len(pb.owned_indices)), int(len(pb.ghost_indices))])
+    del b
+    part = a[5]
+    idx = np.concatenate([part.owned_indices, part.ghost_indices]).astype(np.int64)
+    ppts, pcols = np.ascontiguousarray(pts[idx]), np.ascontiguousarray(cols[idx])
+    rig = scenes.rig_for_cloud(pts, 28, 16, 2048)  # global rig (runtime.hpp:137)
+    del pts, cols, a
+    cam = rig[37]
+    np.testing.assert_array_equal(api.render_mask(ppts, cam, 2.0, 2.0, ctx=ctx),
+                                  ref.render_mask(ppts, cam, 2.0, 2.0))
+    gt = api.ground_truth_model(ppts, pcols, nn, 0.97, ctx=ctx)
+    views = api.DeviceViews.synthesize(ctx, gt, RenderConfig(), [cam], ppts, True, 2.0, 2.0)
+    view = views.download(0)
+    del views, gt
+    seeds = api.seed_gaussians(ppts, pcols, 3, ctx=ctx).download()
+    model = SplatModel(np.ascontiguousarray(seeds.params))
+    rep = step_parity(ctx, ref, model, view, TrainConfig(iterations=1, seed=6))
+    rep["partition"] = 5
+    rep["owned"], rep["ghosts"] = int(len(part.owned_indices)), int(len(part.ghost_indices))
+    rep["partitions_owned_ghost"] = summary
+    _record("config4_rm", rep)
+    _assert_pass(rep)
