@@ -195,7 +195,8 @@ def step_parity(ctx, ref, model: SplatModel, view, tcfg: TrainConfig = None, sha
         strong &= ~affected[:, None]
         strong &= ~loss_cond[:, sl]
         x, y = da[:, sl], db[:, sl]
-        eps_term = np.abs(y) * eps * tol_g / np.maximum(margin, 1e-300) ** 2
+        with np.errstate(divide="ignore", over="ignore", invalid="ignore"):
+            eps_term = np.abs(y) * eps * tol_g / np.maximum(margin, 1e-150) ** 2
         bad = (np.abs(x - y) > ADAM_RTOL * np.abs(y) + 1e-6 * max(float(np.abs(y).max()), 1e-30)
                + np.where(strong, eps_term, 0.0))
         strong_bad += int((bad & strong).sum())
