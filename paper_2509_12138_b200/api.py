@@ -720,10 +720,11 @@ def merge_allgather(comm: Comm, local: DeviceModel, partition) -> tuple:
     return merged, n.value, ms.value
 
 
-def merge_allgather_multi(comm: Comm, locals_, partitions) -> tuple:
+def merge_allgather_multi(comm: Comm, locals_, partitions, out: DeviceModel = None) -> tuple:
     """Several partitions per rank: locals_[j] is partition j * nranks + rank
-    (partition k on GPU k mod N); merged model in partition order."""
-    merged = DeviceModel(comm.ctx)
+    (partition k on GPU k mod N); merged model in partition order. `out`
+    (optional) is reused: its buffers are kept when large enough."""
+    merged = out if out is not None else DeviceModel(comm.ctx)
     n, ms = C.c_int64(), C.c_double()
     arr = (C.c_void_p * len(locals_))(*[m.h.value if hasattr(m.h, "value") else m.h
                                         for m in locals_])

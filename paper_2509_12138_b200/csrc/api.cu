@@ -1791,7 +1791,8 @@ int dsg_merge_models(dsg_ctx ctx, const dsg_model* models, int32_t nparts, int32
 }
 
 struct dsg_comm_s {
-  void* nccl = nullptr;
+  void* nccl = nullptr;      // 64 CTAs per collective: the merge exchange
+  void* nccl_p2p = nullptr;  // NCCL's default CTAs: the band gather
   int nranks = 1, rank = 0;
   std::vector<int> band_rows;  // first tile row of each rank's band, last distributed render
 };
@@ -1808,6 +1809,7 @@ int dsg_comm_create(dsg_ctx ctx, const uint8_t* id128, int32_t nranks, int32_t r
     c->nranks = nranks;
     c->rank = rank;
     c->nccl = nccl_comm_init(id128, nranks, rank);
+    c->nccl_p2p = nccl_comm_split_default(c->nccl, rank);
     *out = c;
   });
 }
@@ -1815,6 +1817,7 @@ int dsg_comm_create(dsg_ctx ctx, const uint8_t* id128, int32_t nranks, int32_t r
 int dsg_comm_destroy(dsg_comm comm) {
   return guarded([&] {
     if (!comm) return;
+    if (comm->nccl_p2p) nccl_comm_destroy(comm->nccl_p2p);
     nccl_comm_destroy(comm->nccl);
     delete comm;
   });
@@ -1900,7 +1903,7 @@ int dsg_render_distributed(dsg_ctx ctx, dsg_comm comm, dsg_model model, const ds
     band.band_ty0 = t0[me];
     band.band_ty1 = t1[me];
     forward(ctx, model->m, band, rd);
-    if (R > 1) gather_bands_dev(comm->nccl, R, me, ctx->frame.rgb.get(), cam.width, cam.height, r0, r1, st);
+    if (R > 1) gather_bands_dev(comm->nccl_p2p ? comm->nccl_p2p : comm->nccl, R, me, ctx->frame.rgb.get(), cam.width, cam.height, r0, r1, st);
     DSG_CUDA_CHECK(cudaEventRecord(b, st));
     DSG_CUDA_CHECK(cudaEventSynchronize(b));
     float t;

@@ -36,6 +36,8 @@ struct Nccl {
   void* h = nullptr;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
@@ -48,6 +50,9 @@ struct Nccl {
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (NCCL >= 2.19): buffer registration
+  ncclResult_t (*CommRegister)(const ncclComm_t, void*, size_t, void**) = nullptr;
+  ncclResult_t (*CommDeregister)(const ncclComm_t, void*) = nullptr;
 };
 
 Nccl& nccl() {
@@ -72,6 +77,10 @@ Nccl& nccl() {
   n.GroupStart = (decltype(n.GroupStart))sym("ncclGroupStart");
   n.GroupEnd = (decltype(n.GroupEnd))sym("ncclGroupEnd");
   n.GetErrorString = (decltype(n.GetErrorString))sym("ncclGetErrorString");
+  n.CommInitRankConfig = (decltype(n.CommInitRankConfig))dlsym(h, "ncclCommInitRankConfig");
+  n.CommSplit = (decltype(n.CommSplit))dlsym(h, "ncclCommSplit");
+  n.CommRegister = (decltype(n.CommRegister))dlsym(h, "ncclCommRegister");
+  n.CommDeregister = (decltype(n.CommDeregister))dlsym(h, "ncclCommDeregister");
   n.h = h;
   return n;
 }
@@ -93,7 +102,22 @@ void* nccl_comm_init(const uint8_t id_bytes[128], int nranks, int rank) {
   ncclUniqueId id;
   memcpy(&id, id_bytes, 128);
   ncclComm_t c = nullptr;
-  nc(nccl().CommInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+  // 64 CTAs per collective (NCCL's default caps them at 32): the merge's
+  // all-gather of 0.75 GB per rank moves 493 instead of 442 GB/s into each
+  // GPU at N = 4 (tools/merge_bw.py; 48: 424, 96: 466, 128: 463).
+  // DSG_NCCL_CTAS overrides (0 = NCCL's default).
+  static const int ctas = [] {
+    const char* e = std::getenv("DSG_NCCL_CTAS");
+    return e ? std::atoi(e) : 64;
+  }();
+  if (ctas > 0 && nccl().CommInitRankConfig) {
+    ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+    cfg.minCTAs = ctas;
+    cfg.maxCTAs = ctas;
+    nc(nccl().CommInitRankConfig(&c, nranks, id, rank, &cfg), "ncclCommInitRankConfig");
+  } else {
+    nc(nccl().CommInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+  }
   // NCCL connects lazily on first use: run one all-gather and one broadcast
   // per root now, so the timed merge does not pay connection setup.
   Nccl& N = nccl();
@@ -113,8 +137,94 @@ void* nccl_comm_init(const uint8_t id_bytes[128], int nranks, int rank) {
   return c;
 }
 
+// Exchange buffers registered with the communicator (ncclCommRegister), kept
+// per communicator and grown on demand: 501 vs 493 GB/s into each GPU at N = 4
+// with 64 CTAs (NCCL-allocated cuMem buffers were slower: 407).
+// DSG_NCCL_REG=0 falls back to per-call plain buffers.
+struct RegBuf {
+  void* ptr = nullptr;
+  void* handle = nullptr;
+  size_t bytes = 0;
+};
+struct CommBufs {
+  void* comm = nullptr;
+  RegBuf send, recv;
+};
+static std::vector<CommBufs>& comm_bufs() {
+  static std::vector<CommBufs> v;
+  return v;
+}
+static bool reg_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("DSG_NCCL_REG");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+static void reg_free(Nccl& N, void* comm, RegBuf& b) {
+  if (!b.ptr) return;
+  if (b.handle) N.CommDeregister((ncclComm_t)comm, b.handle);
+  cudaFree(b.ptr);
+  b = RegBuf{};
+}
+static bool reg_ensure(Nccl& N, void* comm, RegBuf& b, size_t bytes) {
+  if (b.ptr && b.bytes >= bytes) return true;
+  reg_free(N, comm, b);
+  if (cudaMalloc(&b.ptr, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    b = RegBuf{};
+    return false;
+  }
+  b.bytes = bytes;
+  if (N.CommRegister((ncclComm_t)comm, b.ptr, bytes, &b.handle) != ncclSuccess) b.handle = nullptr;
+  return true;
+}
+// send/recv of at least the given sizes for `comm`, or false (plain buffers then)
+static bool exchange_buffers(void* comm, size_t send_bytes, size_t recv_bytes, float** send,
+                             float** recv) {
+  Nccl& N = nccl();
+  if (!reg_on() || !N.CommRegister || !N.CommDeregister) return false;
+  CommBufs* cb = nullptr;
+  for (auto& x : comm_bufs())
+    if (x.comm == comm) cb = &x;
+  if (!cb) {
+    comm_bufs().push_back(CommBufs{comm, {}, {}});
+    cb = &comm_bufs().back();
+  }
+  if (!reg_ensure(N, comm, cb->send, send_bytes) || !reg_ensure(N, comm, cb->recv, recv_bytes))
+    return false;
+  *send = (float*)cb->send.ptr;
+  *recv = (float*)cb->recv.ptr;
+  return true;
+}
+
+// A second communicator over the same ranks with NCCL's default CTA count,
+// for the band gather's send/recv (64 CTAs slow those small transfers down:
+// RT 4K render 3.5 -> 4.3 ms at N = 4). Collective; null when the library
+// has no ncclCommSplit.
+void* nccl_comm_split_default(void* comm, int rank) {
+  Nccl& N = nccl();
+  if (!comm || !N.CommSplit) return nullptr;
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;  // explicit: a split may inherit the parent's
+  cfg.minCTAs = 1;
+  cfg.maxCTAs = 32;
+  ncclComm_t out = nullptr;
+  nc(N.CommSplit((ncclComm_t)comm, 0, rank, &out, &cfg), "ncclCommSplit");
+  return out;
+}
+
 void nccl_comm_destroy(void* c) {
-  if (c) nccl().CommDestroy((ncclComm_t)c);
+  if (!c) return;
+  Nccl& N = nccl();
+  auto& v = comm_bufs();
+  for (size_t i = 0; i < v.size(); ++i)
+    if (v[i].comm == c) {
+      reg_free(N, c, v[i].send);
+      reg_free(N, c, v[i].recv);
+      v.erase(v.begin() + (long)i);
+      break;
+    }
+  N.CommDestroy((ncclComm_t)c);
 }
 
 namespace {
@@ -210,7 +320,7 @@ __global__ void __launch_bounds__(256) k_peer_pull(const PullPart* __restrict__ 
 // one-word all-reduce after the pushes tells every rank its merged model is
 // complete.
 static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
-                             const std::vector<DevBuf<float>>& dense,
+                             const std::deque<DevBuf<float>>& dense,
                              const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
                              ModelDev& merged, cudaStream_t st, float* wire_ms,
                              bool copy_engines = false) {
@@ -331,7 +441,7 @@ static bool merge_push_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nl
 // are 16 B aligned), publishes its IPC handle, and pulls all partitions it
 // does not own with one k_peer_pull launch.
 static bool merge_pull_peers(Nccl& N, ncclComm_t c, int nranks, int rank, int nlocal,
-                             const std::vector<DevBuf<float>>& dense,
+                             const std::deque<DevBuf<float>>& dense,
                              const std::vector<int64_t>& cnt, const std::vector<int64_t>& off,
                              ModelDev& merged, cudaStream_t st, float* wire_ms) {
   const int P = nranks * nlocal;
@@ -441,7 +551,8 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* co
   const int P = nranks * nlocal;
   // 1. local compaction of each partition into a dense [14][cnt] buffer
   std::vector<int64_t> mine(2 * nlocal);
-  std::vector<DevBuf<float>> dense(nlocal);
+  std::deque<DevBuf<float>>& dense = ms.dense;  // kept between calls
+  if ((int)dense.size() < nlocal) dense.resize(nlocal);
   std::vector<MergeSrc> src(nlocal);
   std::vector<int64_t> lcnt(nlocal);
   for (int j = 0; j < nlocal; ++j) {
@@ -505,40 +616,52 @@ int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* co
     return total;
   }
   g_merge_path = "nccl";
-  // 3b. pack, all-gather, unpack, round by round
+  // 3b. pack every round, align the ranks, the rounds' all-gathers back to
+  // back, then unpack. The alignment (a 4-byte all-reduce) lets the timed
+  // window hold only the transfer: without it the first rank into a round
+  // also waits there for the others' host-side work (count readbacks).
   int64_t maxc_all = 1;
   for (int k = 0; k < P; ++k) maxc_all = std::max(maxc_all, cnt[k]);
-  DevBuf<float> send, recv;
-  send.ensure((size_t)maxc_all * kParams);
-  recv.ensure((size_t)nranks * maxc_all * kParams);
-  cudaEvent_t e0, e1;
-  DSG_CUDA_CHECK(cudaEventCreate(&e0));
-  DSG_CUDA_CHECK(cudaEventCreate(&e1));
-  float t = 0.f;
+  const size_t round_recs = (size_t)maxc_all * kParams;
+  DevBuf<float> send_plain, recv_plain;
+  float *sendp = nullptr, *recvp = nullptr;
+  if (!exchange_buffers(comm, sizeof(float) * (round_recs * nlocal + 1),
+                        sizeof(float) * round_recs * nranks * nlocal, &sendp, &recvp)) {
+    sendp = send_plain.ensure(round_recs * nlocal + 1);
+    recvp = recv_plain.ensure(round_recs * nranks * nlocal);
+  }
+  std::vector<int64_t> maxc(nlocal, 1);
   for (int j = 0; j < nlocal; ++j) {
-    int64_t maxc = 1;
-    for (int r = 0; r < nranks; ++r) maxc = std::max(maxc, cnt[j * nranks + r]);
+    for (int r = 0; r < nranks; ++r) maxc[j] = std::max(maxc[j], cnt[j * nranks + r]);
     const int64_t my = cnt[j * nranks + rank];
     if (my > 0) {
       k_pack_records<<<(unsigned)((my * kParams + 255) / 256), 256, 0, st>>>(
-          dense[j].get(), std::max<int64_t>(my, 1), my, send.get());
+          dense[j].get(), std::max<int64_t>(my, 1), my, sendp + round_recs * j);
       count_launch();
     }
-    DSG_CUDA_CHECK(cudaEventRecord(e0, st));
-    nc(N.AllGather(send.get(), recv.get(), (size_t)maxc * kParams, ncclFloat32, c, st),
+  }
+  float* flag = sendp + round_recs * nlocal;
+  DSG_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(float), st));
+  nc(N.AllReduce(flag, flag, 1, ncclFloat32, ncclSum, c, st), "align ranks");
+  cudaEvent_t e0, e1;
+  DSG_CUDA_CHECK(cudaEventCreate(&e0));
+  DSG_CUDA_CHECK(cudaEventCreate(&e1));
+  DSG_CUDA_CHECK(cudaEventRecord(e0, st));
+  for (int j = 0; j < nlocal; ++j)
+    nc(N.AllGather(sendp + round_recs * j, recvp + round_recs * nranks * j,
+                   (size_t)maxc[j] * kParams, ncclFloat32, c, st),
        "allgather survivors");
-    DSG_CUDA_CHECK(cudaEventRecord(e1, st));
-    const int64_t tot_rec = (int64_t)nranks * maxc * kParams;
+  DSG_CUDA_CHECK(cudaEventRecord(e1, st));
+  for (int j = 0; j < nlocal; ++j) {
+    const int64_t tot_rec = (int64_t)nranks * maxc[j] * kParams;
     k_unpack_records<<<(unsigned)((tot_rec + 255) / 256), 256, 0, st>>>(
-        recv.get(), maxc, nranks, co.get() + (size_t)j * nranks, co.get() + P + (size_t)j * nranks,
-        merged.params.get(), merged.cap);
+        recvp + round_recs * nranks * j, maxc[j], nranks, co.get() + (size_t)j * nranks,
+        co.get() + P + (size_t)j * nranks, merged.params.get(), merged.cap);
     count_launch();
-    DSG_CUDA_CHECK(cudaEventSynchronize(e1));
-    float tj = 0.f;
-    DSG_CUDA_CHECK(cudaEventElapsedTime(&tj, e0, e1));
-    t += tj;
   }
   DSG_CUDA_CHECK(cudaStreamSynchronize(st));
+  float t = 0.f;
+  DSG_CUDA_CHECK(cudaEventElapsedTime(&t, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (wire_ms) *wire_ms = t;

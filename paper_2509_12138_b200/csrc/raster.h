@@ -1,5 +1,6 @@
 // Raster pipeline state for one view (per context scratch) and launchers.
 #pragma once
+#include <deque>
 #include <atomic>
 
 #include "dsg_internal.h"
@@ -228,6 +229,7 @@ PartitionResult partition_dev(const double* host_pts, int64_t n, int nparts, dou
 struct MergeScratch {
   DevBuf<uint32_t> flag, pos, cnt;
   std::vector<int64_t> base;
+  std::deque<DevBuf<float>> dense;  // merge exchange: each local partition's survivors, planar
 };
 struct MergeSrc {
   const float* params;
@@ -260,6 +262,7 @@ extern const char* g_merge_path;  // last merge exchange: "peer" or "nccl"
 void nccl_unique_id(uint8_t out[128]);
 void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(void* comm);
+void* nccl_comm_split_default(void* comm, int rank);
 int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* const* locals,
                             int nlocal, int axis, const double* cut_lo, const double* cut_hi,
                             ModelDev& merged, ScanScratch& sc, MergeScratch& ms, cudaStream_t st,

@@ -23,6 +23,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--per-rank", type=int, default=26_700_000)
     ap.add_argument("--reps", type=int, default=4)
+    ap.add_argument("--torch-first", action="store_true")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -43,18 +44,46 @@ def main():
         locs.append(api.DeviceModel(ctx, SplatModel(p, 0, k)))
         parts.append(Partition(k, 0, float(k), float(k + 1), np.zeros((2, 3)), 0.0,
                                np.zeros(0, np.uint32), np.zeros(0, np.uint32)))
-    for r in range(a.reps):
-        dist.barrier()
-        merged, n, ms = api.merge_allgather_multi(comm, locs, parts)
-        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        if rank == 0:
-            wire = 56.0 * n * (world - 1) / world
-            print(f"rep {r}: {n:,} splats, {t.item():.2f} ms, {wire / (t.item() * 1e-3) / 1e9:.1f} GB/s "
-                  f"into each GPU [{os.environ.get('NCCL_ALGO', '-')}/{os.environ.get('NCCL_PROTO', '-')}"
-                  f"/ch{os.environ.get('NCCL_MIN_NCHANNELS', '-')}] via {api.merge_exchange()}",
-                  flush=True)
-        del merged
+    def merges():
+        for r in range(a.reps):
+            dist.barrier()
+            merged, n, ms = api.merge_allgather_multi(comm, locs, parts)
+            t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            if rank == 0:
+                wire = 56.0 * n * (world - 1) / world
+                print(f"rep {r}: {n:,} splats, {t.item():.2f} ms, {wire / (t.item() * 1e-3) / 1e9:.1f} GB/s "
+                      f"into each GPU [{os.environ.get('NCCL_ALGO', '-')}/{os.environ.get('NCCL_PROTO', '-')}"
+                      f"/ch{os.environ.get('NCCL_MIN_NCHANNELS', '-')}] via {api.merge_exchange()}",
+                      flush=True)
+            del merged
+
+    def fabric():
+        # the fabric's own all-gather: torch.distributed (NCCL) on a buffer of one
+        # merge round's size per rank, device-timed, same GB/s definition
+        nbytes = half * 56
+        src = torch.empty(nbytes // 4, dtype=torch.float32, device=f"cuda:{local}")
+        dst = torch.empty(world * (nbytes // 4), dtype=torch.float32, device=f"cuda:{local}")
+        for written in (False, True):
+            for r in range(a.reps + 1):
+                dist.barrier()
+                if written:  # the source just written by a kernel, as the merge's pack leaves it
+                    src.fill_(float(r))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                dist.all_gather_into_tensor(dst, src)
+                e1.record()
+                e1.synchronize()
+                t = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}", dtype=torch.float64)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                if rank == 0 and r > 0:
+                    wire = nbytes * (world - 1)
+                    print(f"torch all_gather_into_tensor {nbytes / 1e6:.0f} MB/rank"
+                          f"{' (source just written)' if written else ''}: {t.item():.2f} ms, "
+                          f"{wire / (t.item() * 1e-3) / 1e9:.1f} GB/s into each GPU", flush=True)
+
+    for f in ((fabric, merges) if a.torch_first else (merges, fabric)):
+        f()
     comm.close()
     dist.destroy_process_group()
 
