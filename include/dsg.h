@@ -292,6 +292,12 @@ int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* local
  * copy-engine plane copies); a peer variant falls back to NCCL when IPC is
  * unavailable. */
 const char* dsg_merge_exchange(void);
+/* Diagnostic: `reps` NCCL all-gathers of `bytes` per rank on the merge
+ * exchange communicator (plain device buffers), each bracketed by CUDA
+ * events after a rank alignment; *ms = the mean device time per
+ * all-gather. Collective over the communicator's ranks. */
+int dsg_comm_bench_allgather(dsg_ctx ctx, dsg_comm comm, int64_t bytes, int32_t reps,
+                             double* ms);
 /* Tile-parallel render (comm may be NULL): rank r bins and blends tile-row
  * band r of the replicated model, the bands cut at the quantiles of the
  * splats' projected centres per tile row (computed identically on every

@@ -736,6 +736,15 @@ def merge_allgather_multi(comm: Comm, locals_, partitions, out: DeviceModel = No
     return merged, n.value, ms.value
 
 
+def bench_allgather(comm: Comm, nbytes: int, reps: int = 3) -> float:
+    """Diagnostic: mean device ms of an all-gather of `nbytes` per rank on the
+    exchange communicator (dsg_comm_bench_allgather). Collective."""
+    ms = C.c_double()
+    _check(lib().dsg_comm_bench_allgather(comm.ctx.h, comm.h, C.c_int64(nbytes), C.c_int32(reps),
+                                          C.byref(ms)))
+    return ms.value
+
+
 def merge_exchange() -> str:
     """'peer' (NVLink pulls through CUDA IPC) or 'nccl' for the last merge."""
     L = lib()

@@ -1849,6 +1849,16 @@ int dsg_merge_allgather_multi(dsg_ctx ctx, dsg_comm comm, const dsg_model* local
 
 const char* dsg_merge_exchange(void) { return dsg::g_merge_path; }
 
+int dsg_comm_bench_allgather(dsg_ctx ctx, dsg_comm comm, int64_t bytes, int32_t reps,
+                             double* ms) {
+  return guarded([&] {
+    if (!comm || bytes < 4 || reps < 1) fail(kInvalidArgument, "bench_allgather: bad arguments");
+    DeviceGuard g(ctx->device);
+    const double t = bench_allgather_dev(comm->nccl, comm->nranks, bytes, reps, ctx->stream);
+    if (ms) *ms = t;
+  });
+}
+
 int dsg_merge_allgather(dsg_ctx ctx, dsg_comm comm, dsg_model local, int32_t axis, double cut_lo,
                         double cut_hi, dsg_model merged, int64_t* n_merged, double* ms) {
   return dsg_merge_allgather_multi(ctx, comm, &local, 1, axis, &cut_lo, &cut_hi, merged, n_merged,

@@ -263,6 +263,7 @@ void nccl_unique_id(uint8_t out[128]);
 void* nccl_comm_init(const uint8_t id[128], int nranks, int rank);
 void nccl_comm_destroy(void* comm);
 void* nccl_comm_split_default(void* comm, int rank);
+double bench_allgather_dev(void* comm, int nranks, int64_t bytes, int reps, cudaStream_t st);
 int64_t merge_allgather_dev(void* comm, int nranks, int rank, const ModelDev* const* locals,
                             int nlocal, int axis, const double* cut_lo, const double* cut_hi,
                             ModelDev& merged, ScanScratch& sc, MergeScratch& ms, cudaStream_t st,

@@ -82,7 +82,17 @@ def main():
                           f"{' (source just written)' if written else ''}: {t.item():.2f} ms, "
                           f"{wire / (t.item() * 1e-3) / 1e9:.1f} GB/s into each GPU", flush=True)
 
-    for f in ((fabric, merges) if a.torch_first else (merges, fabric)):
+    def raw():
+        # the exchange communicator's own all-gather on plain buffers
+        nbytes = half * 56
+        ms = api.bench_allgather(comm, nbytes, a.reps)
+        t = torch.tensor([ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            print(f"libdsg communicator all-gather {nbytes / 1e6:.0f} MB/rank: {t.item():.2f} ms, "
+                  f"{nbytes * (world - 1) / (t.item() * 1e-3) / 1e9:.1f} GB/s into each GPU", flush=True)
+
+    for f in ((fabric, merges, raw) if a.torch_first else (merges, fabric, raw)):
         f()
     comm.close()
     dist.destroy_process_group()
