@@ -20,6 +20,7 @@
 #include <cstring>
 #include <nccl.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -154,6 +155,10 @@ static std::vector<CommBufs>& comm_bufs() {
   static std::vector<CommBufs> v;
   return v;
 }
+static std::mutex& comm_bufs_mu() {
+  static std::mutex m;
+  return m;
+}
 static bool reg_on() {
   static const bool on = [] {
     const char* e = std::getenv("DSG_NCCL_REG");
@@ -184,6 +189,7 @@ static bool exchange_buffers(void* comm, size_t send_bytes, size_t recv_bytes, f
                              float** recv) {
   Nccl& N = nccl();
   if (!reg_on() || !N.CommRegister || !N.CommDeregister) return false;
+  std::lock_guard<std::mutex> lk(comm_bufs_mu());
   CommBufs* cb = nullptr;
   for (auto& x : comm_bufs())
     if (x.comm == comm) cb = &x;
@@ -216,6 +222,7 @@ void* nccl_comm_split_default(void* comm, int rank) {
 void nccl_comm_destroy(void* c) {
   if (!c) return;
   Nccl& N = nccl();
+  std::lock_guard<std::mutex> lk(comm_bufs_mu());
   auto& v = comm_bufs();
   for (size_t i = 0; i < v.size(); ++i)
     if (v[i].comm == c) {
