@@ -143,6 +143,11 @@ __global__ void __launch_bounds__(256, DSG_PRE_MINB) k_preprocess(PreprocessArgs
 // within range / 2^bits) are put in (depth, index) order by the fix-up below;
 // 24 bits saves a pass at N=1 but makes long near-coincident runs (and their
 // radix-sort fallback) far more frequent in sparse partition views.
+// Backward partial rows keyed by splat index (1) or by duplicate emission
+// position (0); see bin_frame.
+#ifndef DSG_ROWS_BY_INDEX
+#define DSG_ROWS_BY_INDEX 1
+#endif
 #ifndef DSG_DEPTH_KEY_BITS
 #define DSG_DEPTH_KEY_BITS 32
 #endif
@@ -320,7 +325,7 @@ __global__ void k_duplicate(const uint32_t* __restrict__ vis_idx, int64_t nv,
   if (s >= nv) return;
   uint32_t i = vis_idx[s];
   uint32_t o = offs[s];
-  dup_base[i] = o;
+  if (dup_base) dup_base[i] = o;  // partial rows in emission (depth) order
   const int4 pr = trect[i];
   MaskSplat ms;
   ms.er = erect[i];
@@ -524,7 +529,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
   f.tcount.ensure(std::max<int64_t>(n, 1));
   f.depth.ensure(std::max<int64_t>(n, 1));
   f.exact.ensure(3 * (size_t)std::max<int64_t>(n, 1));
-  f.dup_base.ensure(std::max<int64_t>(n, 1));
+  f.dup_base.ensure(std::max<int64_t>(n, 1) + 1);
   f.vis_key.ensure(std::max<int64_t>(n, 1));
   f.vis_idx.ensure(std::max<int64_t>(n, 1));
   f.vis_key2.ensure(std::max<int64_t>(n, 1));
@@ -555,7 +560,15 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
     pdl_launch(k_preprocess, blocks(n, 256), 256, 0, st, a);
     count_launch();
     DSG_CUDA_CHECK(cudaGetLastError());
+#if DSG_ROWS_BY_INDEX
+    // Visible-slot scan, and the backward partial rows keyed by splat index
+    // (K6 writes them, K7 reads them): row base of splat i = its tiles'
+    // running count in index order, so K7's threads (consecutive splats)
+    // read consecutive rows (chain + Adam 0.63 -> 0.58 ms). One dual pass.
+    exclusive_scan_u32_dual(f.tcount.get(), f.vslot.get(), f.dup_base.get(), n, f.scan, st);
+#else
     exclusive_scan_u32(f.tcount.get(), f.vslot.get(), n, f.scan, st, true);
+#endif
     pdl_launch(k_vis_compact, blocks(n, 256), 256, 0, st, f.tcount.get(), f.depth.get(), f.drange.get(),
                                                   f.vslot.get(), n, f.vis_key.get(),
                                                   f.vis_idx.get());
@@ -649,7 +662,7 @@ void bin_frame(Frame& f, const float* params, int64_t pitch, int64_t n, const Ca
                                                g_exact_masks.load() != 0,
                                                cam.tiles_x, cam.band_ty0, cam.band_ty1,
                                                f.tile_key.get(), f.dup_val.get(),
-                                               f.dup_base.get());
+                                               DSG_ROWS_BY_INDEX ? nullptr : f.dup_base.get());
   count_launch();
   tm.mark(3, st);
   int tile_bits = 1;

@@ -85,5 +85,9 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
 // flags: sum (in[i] != 0) instead of in[i] (order-preserving compaction).
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratch& s,
                         cudaStream_t st, bool flags = false);
+// Both scans of one input in one pass: out_flags = scan of (in[i] != 0),
+// out_vals = scan of in[i] (each with the total at [n]; totals < 2^32).
+void exclusive_scan_u32_dual(const uint32_t* in, uint32_t* out_flags, uint32_t* out_vals,
+                             int64_t n, ScanScratch& s, cudaStream_t st);
 
 }  // namespace dsg

@@ -389,7 +389,93 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_down(const uint32_t* __re
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) out[n] = sums[gridDim.x];
 }
 
+// Dual scan: (in[i] != 0) and in[i] summed together as one u64, the flag
+// count in the high word (the low word's running sum never exceeds the u32
+// total, so it never carries).
+using u64 = unsigned long long;
+__device__ __forceinline__ u64 pack2(uint32_t v) { return ((u64)(v != 0) << 32) | v; }
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_reduce2(const uint32_t* __restrict__ in,
+                                                               int64_t n, u64* sums) {
+  DSG_PDL_ENTRY();
+  __shared__ u64 tmp[33];
+  int64_t base = (int64_t)blockIdx.x * kScanTile;
+  u64 s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    int64_t idx = base + (int64_t)i * kScanThreads + threadIdx.x;
+    if (idx < n) s += pack2(in[idx]);
+  }
+  u64 agg;
+  block_exclusive_sum<kScanThreads>(s, &agg, tmp);
+  if (threadIdx.x == 0) sums[blockIdx.x] = agg;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_sums2(u64* sums, int64_t nb) {
+  DSG_PDL_ENTRY();
+  __shared__ u64 tmp[33];
+  __shared__ u64 carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nb; base += 1024) {
+    int64_t i = base + threadIdx.x;
+    u64 v = i < nb ? sums[i] : 0ull, agg;
+    u64 ex = block_exclusive_sum<1024>(v, &agg, tmp);
+    if (i < nb) sums[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += agg;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sums[nb] = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_down2(const uint32_t* __restrict__ in,
+                                                             uint32_t* out_f, uint32_t* out_v,
+                                                             int64_t n, const u64* __restrict__ sums) {
+  DSG_PDL_ENTRY();
+  __shared__ u64 tmp[33];
+  int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  u64 local = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    v[i] = (base + i < n) ? in[base + i] : 0u;
+    local += pack2(v[i]);
+  }
+  u64 agg;
+  u64 run = block_exclusive_sum<kScanThreads>(local, &agg, tmp) + sums[blockIdx.x];
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) {
+      out_f[base + i] = (uint32_t)(run >> 32);
+      out_v[base + i] = (uint32_t)run;
+    }
+    run += pack2(v[i]);
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+    out_f[n] = (uint32_t)(sums[gridDim.x] >> 32);
+    out_v[n] = (uint32_t)sums[gridDim.x];
+  }
+}
+
 }  // namespace
+
+void exclusive_scan_u32_dual(const uint32_t* in, uint32_t* out_flags, uint32_t* out_vals,
+                             int64_t n, ScanScratch& s, cudaStream_t st) {
+  if (n <= 0) {
+    DSG_CUDA_CHECK(cudaMemsetAsync(out_flags, 0, sizeof(uint32_t), st));
+    DSG_CUDA_CHECK(cudaMemsetAsync(out_vals, 0, sizeof(uint32_t), st));
+    return;
+  }
+  int64_t nb = (n + kScanTile - 1) / kScanTile;
+  u64* sums = reinterpret_cast<u64*>(s.block_sums.ensure(2 * (nb + 1)));
+  pdl_launch(k_scan_reduce2, (unsigned)nb, kScanThreads, 0, st, in, n, sums);
+  pdl_launch(k_scan_sums2, 1, 1024, 0, st, sums, nb);
+  pdl_launch(k_scan_down2, (unsigned)nb, kScanThreads, 0, st, in, out_flags, out_vals, n,
+             (const u64*)sums);
+  count_launch(3);
+  DSG_CUDA_CHECK(cudaGetLastError());
+}
 
 void exclusive_scan_u32(const uint32_t* in, uint32_t* out, int64_t n, ScanScratch& s,
                         cudaStream_t st, bool flags) {
